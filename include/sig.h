@@ -1,0 +1,163 @@
+/*
+ * sig.h -- C ABI of libsig.so, the B200 (sm_100a) hot path of Signatory (arXiv 2001.00706):
+ * batched truncated signature / logsignature transforms of piecewise-linear paths, their
+ * handwritten reversible backward passes, and the group-like product.
+ *
+ * Citations "P:Lnnn" are lines of the paper's LaTeX source (reference PAPER.md).
+ *
+ * Conventions for every call
+ *  - Tensors are DEVICE pointers to contiguous, row-major float32 arrays, owned by the caller
+ *    (allocated through PyTorch in the Python binding).  The library never allocates device
+ *    memory on these calls and writes only to the output / gradient / workspace arguments.
+ *  - Every call is asynchronous on the given CUDA stream (cudaStream_t, may be NULL = legacy
+ *    default stream).  Errors in the arguments are detected on the host BEFORE anything is
+ *    launched and reported as SIG_ERR_INVALID_ARG / SIG_ERR_SHAPE; a (C, depth) pair for which
+ *    no kernel is compiled returns SIG_ERR_UNSUPPORTED (there is no CPU fallback); a failed
+ *    launch returns SIG_ERR_CUDA.  NaN/Inf inputs are not checked and propagate.  A detail
+ *    string for the last error of the calling thread is available from sig_last_error().
+ *  - Truncated tensor layout: levels k = 1..depth back to back; inside
+ *    level k the word (j_1..j_k) (0-based channel letters) is at offset sum_m j_m C^(k-m).
+ *    The scalar level 0 is not stored: it is 1 for signatures, 0 for logsignatures.
+ *    S = sig_signature_channels(C, depth) = sum_{k=1}^{depth} C^k floats per path.
+ *  - Paths are [B, L, C]: B streams of L points in R^C.  The path is the
+ *    piecewise-linear interpolation of its points; increments z_t = x_{t+1} - x_t.
+ *  - basepoint (reading R4): SIG_BP_NONE uses the points as given;
+ *    SIG_BP_ZERO prepends the origin; SIG_BP_GIVEN prepends basepoint[b] ([B, C] device array).
+ *    With a basepoint the stream has L+1 points (so L >= 1 suffices); without, L >= 2.
+ *    M = L - 1 (+1 with a basepoint) is the number of increments.
+ *  - stream: 0 returns Sig of the whole path, [B, S]; 1 returns every expanding
+ *    prefix Sig(x_1..x_{j+1}), j = 1..M, as [B, M, S].
+ *  - Results are deterministic: every reduction has a fixed order.
+ */
+#ifndef SIG_B200_H
+#define SIG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sig_cuda_stream_t; /* identical to cudaStream_t */
+
+typedef enum {
+    SIG_OK = 0,
+    SIG_ERR_INVALID_ARG = 1, /* null pointer, C < 1, depth < 1, bad enum */
+    SIG_ERR_SHAPE = 2,       /* too few points, sizes overflow int64, workspace too small */
+    SIG_ERR_UNSUPPORTED = 3, /* no sm_100a kernel instantiated for (C, depth) or path too long */
+    SIG_ERR_CUDA = 4,        /* a CUDA launch or runtime call failed */
+    SIG_ERR_WORKSPACE = 5    /* ws_bytes smaller than the size the *_workspace_size query gave */
+} sig_status_t;
+
+typedef enum { SIG_BP_NONE = 0, SIG_BP_ZERO = 1, SIG_BP_GIVEN = 2 } sig_basepoint_t;
+
+/* Logsignature bases (Appendix A.2):
+ *  EXPAND   -- log Sig itself in the tensor basis, S floats.
+ *  BRACKETS -- coefficients alpha_l of the Lyndon basis phi(l): sum_l alpha_l phi(l) = log Sig
+ *              (eq-linearsystem), w(C, depth) floats.
+ *  WORDS    -- the paper's new basis z = psi(log Sig): the coefficients of the Lyndon words
+ *              (P:L561-575), w(C, depth) floats.  Lyndon words are ordered by (length, lex).   */
+typedef enum { SIG_LOGSIG_EXPAND = 0, SIG_LOGSIG_BRACKETS = 1, SIG_LOGSIG_WORDS = 2 } sig_logsig_mode_t;
+
+/* ---------------------------------------------------------------- sizes and diagnostics */
+
+/* S = sum_{k=1}^{depth} C^k; -1 if C < 1, depth < 1 or the sum overflows int64. */
+int64_t sig_signature_channels(int64_t C, int32_t depth);
+
+/* Output width of the logsignature: S for EXPAND, Witt's formula w(C, depth) for
+ * BRACKETS and WORDS; -1 on invalid arguments. */
+int64_t sig_logsignature_channels(int64_t C, int32_t depth, sig_logsig_mode_t mode);
+
+/* 1 if sm_100a kernels exist for (C, depth) -- forward (backward = 0) or backward (backward = 1);
+ * 0 otherwise. */
+int32_t sig_is_supported(int64_t C, int32_t depth, int32_t backward);
+
+/* Number of CUDA kernels this library has launched in this process (all devices and threads) --
+ * a diagnostic used by the benchmark to report how many of its own kernels ran. */
+uint64_t sig_launch_count(void);
+
+const char* sig_status_string(sig_status_t status);
+/* Detail of the last failed call on this host thread ("" if none).  Valid until the next call. */
+const char* sig_last_error(void);
+
+/* ---------------------------------------------------------------- signature (K1 + K3) */
+
+/* Bytes of device workspace sig_signature needs for this problem (0 when the whole path of every
+ * stream is scanned by one unit; > 0 when long paths are split into time chunks whose
+ * signatures are then folded in order with Chen's identity). */
+size_t sig_signature_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                                    sig_basepoint_t bp);
+
+/* Forward signature by the fused multiply-exponentiate scan (eq-fusedterm).
+ *   path      [B, L, C]
+ *   basepoint [B, C] if bp == SIG_BP_GIVEN, else ignored (may be NULL)
+ *   out       [B, S] (stream = 0) or [B, M, S] (stream = 1); fully overwritten
+ *   ws        device workspace of at least sig_signature_workspace_size(...) bytes (NULL if 0) */
+sig_status_t sig_signature(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                           sig_basepoint_t bp, const float* basepoint, float* out, void* ws, size_t ws_bytes,
+                           sig_cuda_stream_t s);
+
+/* Reversible backward (Appendix C): gradients of <grad_out, Sig(path)>.
+ *   grad_out       [B, S] or [B, M, S] (stream), the upstream gradient
+ *   out_saved      the forward's `out` for the same arguments (its final signature seeds the
+ *                  reversal eq-reverse); consistency with `path` is NOT checked
+ *   grad_path      [B, L, C], overwritten
+ *   grad_basepoint [B, C] (bp == SIG_BP_GIVEN) or NULL; overwritten when given
+ * Needs the increments of one path in shared memory: M * C <= 32768 floats, else UNSUPPORTED. */
+sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
+                                    int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
+                                    const float* basepoint, float* grad_path, float* grad_basepoint,
+                                    sig_cuda_stream_t s);
+
+/* ---------------------------------------------------------------- combine (K3) */
+
+/* out[b] = a[b] [x] b[b] for b < B; all [B, S]. out must not alias a or b. */
+sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, int64_t C, int32_t depth, float* out,
+                                   sig_cuda_stream_t s);
+
+/* VJP of sig_signature_combine: grad_a, grad_b [B, S] overwritten (either may be NULL). */
+sig_status_t sig_signature_combine_backward(const float* grad_out, const float* a, const float* b, int64_t B,
+                                            int64_t C, int32_t depth, float* grad_a, float* grad_b,
+                                            sig_cuda_stream_t s);
+
+size_t sig_multi_signature_combine_workspace_size(int64_t n, int64_t B, int64_t C, int32_t depth);
+
+/* out[b] = sigs[0, b] [x] sigs[1, b] [x] ... [x] sigs[n-1, b]   (sigs [n, B, S] in time order;
+ * an ordered tree).  n >= 1. */
+sig_status_t sig_multi_signature_combine(const float* sigs, int64_t n, int64_t B, int64_t C, int32_t depth,
+                                         float* out, void* ws, size_t ws_bytes, sig_cuda_stream_t s);
+
+/* ---------------------------------------------------------------- logsignature (K4/K5) */
+
+/* Immutable per-(C, depth, mode) tables (Lyndon words, flat indices, exact integer inverse of
+ * psi o phi for BRACKETS), uploaded to the current device at creation.  A plan may be shared by
+ * threads; destroy it after the last call that uses it has completed on the device. */
+typedef struct sig_logsig_plan_s* sig_logsig_plan_t;
+
+sig_status_t sig_logsig_plan_create(int64_t C, int32_t depth, sig_logsig_mode_t mode, sig_logsig_plan_t* plan);
+sig_status_t sig_logsig_plan_destroy(sig_logsig_plan_t plan);
+
+/* Workspace for sig_logsignature / _backward (includes the signature scan's own workspace). */
+size_t sig_logsignature_workspace_size(sig_logsig_plan_t plan, int64_t B, int64_t L, int32_t stream,
+                                       sig_basepoint_t bp);
+
+/* LogSig = log(Sig(path)) in the plan's basis.
+ *   out        [B, w] (WORDS, BRACKETS) or [B, S] (EXPAND); stream: [B, M, w|S]
+ *   sig_saved  [B, S] | [B, M, S]: receives the signature (needed by the backward); may be NULL
+ *              only if ws is large enough to hold it (then it is written to the workspace) */
+sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t B, int64_t L, int32_t stream,
+                              sig_basepoint_t bp, const float* basepoint, float* out, float* sig_saved, void* ws,
+                              size_t ws_bytes, sig_cuda_stream_t s);
+
+/* Backward of sig_logsignature: grad_out [B, w|S] (| stream [B, M, w|S]); sig_saved from the
+ * forward; grad_path [B, L, C] and grad_basepoint [B, C] (or NULL) overwritten. */
+sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad_out, const float* path,
+                                       const float* sig_saved, int64_t B, int64_t L, int32_t stream,
+                                       sig_basepoint_t bp, const float* basepoint, float* grad_path,
+                                       float* grad_basepoint, void* ws, size_t ws_bytes, sig_cuda_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIG_B200_H */

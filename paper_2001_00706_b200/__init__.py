@@ -1,0 +1,350 @@
+"""sigb200 -- B200-native (sm_100a) signature / logsignature transforms (Signatory, arXiv 2001.00706).
+
+Thin Python binding of libsig.so (include/sig.h).  This module only marshals arguments: it checks
+that tensors are contiguous float32 CUDA tensors, allocates outputs and workspaces with PyTorch,
+and passes raw device pointers plus the current CUDA stream through ctypes.  Every step of the
+computation runs in the library's CUDA kernels; there is no CPU fallback -- importing works
+anywhere, but any call without the built library or without a CUDA device raises.
+
+Two layers:
+  * ``sig_*`` functions with the same names and argument order as the C ABI (no autograd);
+  * differentiable ``signature``, ``logsignature``, ``signature_combine``,
+    ``multi_signature_combine`` (torch.autograd.Function wrappers whose backward calls the
+    handwritten reversible backward kernels).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+__all__ = [
+    "lib", "LIB_PATH", "SigError",
+    "sig_signature_channels", "sig_logsignature_channels", "sig_is_supported",
+    "sig_signature", "sig_signature_backward", "sig_signature_combine", "sig_signature_combine_backward",
+    "sig_multi_signature_combine", "LogSigPlan", "sig_logsignature", "sig_logsignature_backward",
+    "signature", "logsignature", "signature_combine", "multi_signature_combine",
+    "BP_NONE", "BP_ZERO", "BP_GIVEN", "MODES",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsig.so")
+BP_NONE, BP_ZERO, BP_GIVEN = 0, 1, 2
+MODES = {"expand": 0, "brackets": 1, "words": 2}
+
+_c_i64, _c_i32, _c_sz, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t, ctypes.c_void_p
+
+
+class SigError(RuntimeError):
+    pass
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libsig.so (build it with ``python -m paper_2001_00706_b200.build``).  Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise SigError(f"{LIB_PATH} is missing: build it with `python -m paper_2001_00706_b200.build` "
+                               "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            sig = [
+                ("sig_signature_channels", _c_i64, [_c_i64, _c_i32]),
+                ("sig_logsignature_channels", _c_i64, [_c_i64, _c_i32, ctypes.c_int]),
+                ("sig_is_supported", _c_i32, [_c_i64, _c_i32, _c_i32]),
+                ("sig_status_string", ctypes.c_char_p, [ctypes.c_int]),
+                ("sig_launch_count", ctypes.c_uint64, []),
+                ("sig_last_error", ctypes.c_char_p, []),
+                ("sig_signature_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, ctypes.c_int]),
+                ("sig_signature", ctypes.c_int, [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, ctypes.c_int, _vp, _vp,
+                                                 _vp, _c_sz, _vp]),
+                ("sig_signature_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32,
+                                                          ctypes.c_int, _vp, _vp, _vp, _vp]),
+                ("sig_signature_combine", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _vp]),
+                ("sig_signature_combine_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _vp,
+                                                                  _vp]),
+                ("sig_multi_signature_combine_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32]),
+                ("sig_multi_signature_combine", ctypes.c_int, [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _c_sz,
+                                                               _vp]),
+                ("sig_logsig_plan_create", ctypes.c_int, [_c_i64, _c_i32, ctypes.c_int, ctypes.POINTER(_vp)]),
+                ("sig_logsig_plan_destroy", ctypes.c_int, [_vp]),
+                ("sig_logsignature_workspace_size", _c_sz, [_vp, _c_i64, _c_i64, _c_i32, ctypes.c_int]),
+                ("sig_logsignature", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i32, ctypes.c_int, _vp, _vp, _vp,
+                                                    _vp, _c_sz, _vp]),
+                ("sig_logsignature_backward", ctypes.c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _c_i32, ctypes.c_int,
+                                                             _vp, _vp, _vp, _vp, _c_sz, _vp]),
+            ]
+            for name, res, args in sig:
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        L = lib()
+        raise SigError(f"{what}: {L.sig_status_string(status).decode()}: {L.sig_last_error().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise SigError(f"{name} must be a CUDA tensor (sm_100a kernels only; no CPU fallback)")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    return t.contiguous()
+
+
+def _bp(basepoint, path):
+    """basepoint: None/False -> NONE; True -> ZERO; tensor [B, C] -> GIVEN (reading R4)."""
+    if basepoint is None or basepoint is False:
+        return BP_NONE, None
+    if basepoint is True:
+        return BP_ZERO, None
+    bp = _dev_f32(basepoint, "basepoint")
+    if bp.dim() == 1:
+        bp = bp.unsqueeze(0).expand(path.shape[0], -1).contiguous()
+    return BP_GIVEN, bp
+
+
+# ------------------------------------------------------------------------------------------------
+# C-ABI mirrors
+# ------------------------------------------------------------------------------------------------
+def sig_signature_channels(C: int, depth: int) -> int:
+    return int(lib().sig_signature_channels(C, depth))
+
+
+def sig_logsignature_channels(C: int, depth: int, mode: str = "words") -> int:
+    return int(lib().sig_logsignature_channels(C, depth, MODES[mode]))
+
+
+def sig_is_supported(C: int, depth: int, backward: bool = False) -> bool:
+    return bool(lib().sig_is_supported(C, depth, int(backward)))
+
+
+def sig_signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None) -> torch.Tensor:
+    path = _dev_f32(path, "path")
+    B, L, C = path.shape
+    bpm, bp = _bp(basepoint, path)
+    Lib = lib()
+    S = Lib.sig_signature_channels(C, depth)
+    if S < 0:
+        raise SigError(f"bad C={C} depth={depth}")
+    M = L - 1 + (bpm != BP_NONE)
+    out = torch.empty((B, M, S) if stream else (B, S), device=path.device, dtype=torch.float32)
+    wsb = Lib.sig_signature_workspace_size(B, L, C, depth, int(stream), bpm)
+    ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_signature(_ptr(path), B, L, C, depth, int(stream), bpm, _ptr(bp), _ptr(out), _ptr(ws), wsb,
+                             _stream(path.device)), "sig_signature")
+    return out
+
+
+def sig_signature_backward(grad_out, path, out_saved, depth: int, stream: bool = False, basepoint=None):
+    path = _dev_f32(path, "path")
+    grad_out = _dev_f32(grad_out, "grad_out")
+    out_saved = _dev_f32(out_saved, "out_saved")
+    B, L, C = path.shape
+    bpm, bp = _bp(basepoint, path)
+    gp = torch.empty_like(path)
+    gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
+    _check(lib().sig_signature_backward(_ptr(grad_out), _ptr(path), _ptr(out_saved), B, L, C, depth, int(stream), bpm,
+                                        _ptr(bp), _ptr(gp), _ptr(gbp), _stream(path.device)),
+           "sig_signature_backward")
+    return gp, gbp
+
+
+def sig_signature_combine(a, b, C: int, depth: int):
+    a, b = _dev_f32(a, "a"), _dev_f32(b, "b")
+    out = torch.empty_like(a)
+    _check(lib().sig_signature_combine(_ptr(a), _ptr(b), a.shape[0], C, depth, _ptr(out), _stream(a.device)),
+           "sig_signature_combine")
+    return out
+
+
+def sig_signature_combine_backward(grad_out, a, b, C: int, depth: int):
+    grad_out, a, b = _dev_f32(grad_out, "grad_out"), _dev_f32(a, "a"), _dev_f32(b, "b")
+    ga, gb = torch.empty_like(a), torch.empty_like(b)
+    _check(lib().sig_signature_combine_backward(_ptr(grad_out), _ptr(a), _ptr(b), a.shape[0], C, depth, _ptr(ga),
+                                                _ptr(gb), _stream(a.device)), "sig_signature_combine_backward")
+    return ga, gb
+
+
+def sig_multi_signature_combine(sigs, C: int, depth: int):
+    """sigs [n, B, S] in time order -> [B, S]."""
+    sigs = _dev_f32(sigs, "sigs")
+    n, B, S = sigs.shape
+    Lib = lib()
+    out = torch.empty((B, S), device=sigs.device, dtype=torch.float32)
+    wsb = Lib.sig_multi_signature_combine_workspace_size(n, B, C, depth)
+    ws = torch.empty(wsb, device=sigs.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_multi_signature_combine(_ptr(sigs), n, B, C, depth, _ptr(out), _ptr(ws), wsb,
+                                           _stream(sigs.device)), "sig_multi_signature_combine")
+    return out
+
+
+class LogSigPlan:
+    """Owns a sig_logsig_plan_t (device tables for one (C, depth, mode)), per device."""
+
+    _cache: dict = {}
+
+    def __init__(self, C: int, depth: int, mode: str = "words"):
+        self.C, self.depth, self.mode = C, depth, mode
+        self.handle = ctypes.c_void_p()
+        _check(lib().sig_logsig_plan_create(C, depth, MODES[mode], ctypes.byref(self.handle)),
+               "sig_logsig_plan_create")
+        self.width = sig_logsignature_channels(C, depth, mode)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().sig_logsig_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+    @classmethod
+    def get(cls, C: int, depth: int, mode: str, device) -> "LogSigPlan":
+        key = (C, depth, mode, torch.device(device).index)
+        if key not in cls._cache:
+            with torch.cuda.device(device):
+                cls._cache[key] = LogSigPlan(C, depth, mode)
+        return cls._cache[key]
+
+
+def sig_logsignature(path, depth: int, mode: str = "words", stream: bool = False, basepoint=None,
+                     return_signature: bool = False):
+    path = _dev_f32(path, "path")
+    B, L, C = path.shape
+    plan = LogSigPlan.get(C, depth, mode, path.device)
+    bpm, bp = _bp(basepoint, path)
+    Lib = lib()
+    M = L - 1 + (bpm != BP_NONE)
+    S = sig_signature_channels(C, depth)
+    out = torch.empty((B, M, plan.width) if stream else (B, plan.width), device=path.device, dtype=torch.float32)
+    sig = torch.empty((B, M, S) if stream else (B, S), device=path.device, dtype=torch.float32)
+    wsb = Lib.sig_logsignature_workspace_size(plan.handle, B, L, int(stream), bpm)
+    ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_logsignature(plan.handle, _ptr(path), B, L, int(stream), bpm, _ptr(bp), _ptr(out), _ptr(sig),
+                                _ptr(ws), wsb, _stream(path.device)), "sig_logsignature")
+    return (out, sig) if return_signature else out
+
+
+def sig_logsignature_backward(grad_out, path, sig_saved, depth: int, mode: str = "words", stream: bool = False,
+                              basepoint=None):
+    path = _dev_f32(path, "path")
+    grad_out = _dev_f32(grad_out, "grad_out")
+    sig_saved = _dev_f32(sig_saved, "sig_saved")
+    B, L, C = path.shape
+    plan = LogSigPlan.get(C, depth, mode, path.device)
+    bpm, bp = _bp(basepoint, path)
+    Lib = lib()
+    gp = torch.empty_like(path)
+    gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
+    wsb = Lib.sig_logsignature_workspace_size(plan.handle, B, L, int(stream), bpm)
+    ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_logsignature_backward(plan.handle, _ptr(grad_out), _ptr(path), _ptr(sig_saved), B, L, int(stream),
+                                         bpm, _ptr(bp), _ptr(gp), _ptr(gbp), _ptr(ws), wsb, _stream(path.device)),
+           "sig_logsignature_backward")
+    return gp, gbp
+
+
+# ------------------------------------------------------------------------------------------------
+# differentiable API (Signatory-style)
+# ------------------------------------------------------------------------------------------------
+class _Signature(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, path, depth, stream, basepoint_flag, bp_tensor):
+        bp = bp_tensor if basepoint_flag == BP_GIVEN else (basepoint_flag == BP_ZERO)
+        out = sig_signature(path, depth, stream, bp)
+        ctx.save_for_backward(path, out, bp_tensor if basepoint_flag == BP_GIVEN else None)
+        ctx.depth, ctx.stream, ctx.bpf = depth, stream, basepoint_flag
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        path, out, bpt = ctx.saved_tensors
+        bp = bpt if ctx.bpf == BP_GIVEN else (ctx.bpf == BP_ZERO)
+        gp, gbp = sig_signature_backward(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp)
+        return gp, None, None, None, gbp
+
+
+def _bp_args(basepoint):
+    if basepoint is None or basepoint is False:
+        return BP_NONE, None
+    if basepoint is True:
+        return BP_ZERO, None
+    return BP_GIVEN, basepoint
+
+
+def signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None) -> torch.Tensor:
+    """Sig^depth of each stream in path [B, L, C] -> [B, S] (or [B, M, S] with stream=True).
+    Differentiable; the backward is the reversible handwritten kernel."""
+    f, t = _bp_args(basepoint)
+    return _Signature.apply(path, depth, stream, f, t)
+
+
+class _LogSignature(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, path, depth, mode, stream, basepoint_flag, bp_tensor):
+        bp = bp_tensor if basepoint_flag == BP_GIVEN else (basepoint_flag == BP_ZERO)
+        out, sig = sig_logsignature(path, depth, mode, stream, bp, return_signature=True)
+        ctx.save_for_backward(path, sig, bp_tensor if basepoint_flag == BP_GIVEN else None)
+        ctx.depth, ctx.mode, ctx.stream, ctx.bpf = depth, mode, stream, basepoint_flag
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        path, sig, bpt = ctx.saved_tensors
+        bp = bpt if ctx.bpf == BP_GIVEN else (ctx.bpf == BP_ZERO)
+        gp, gbp = sig_logsignature_backward(grad_out.contiguous(), path, sig, ctx.depth, ctx.mode, ctx.stream, bp)
+        return gp, None, None, None, None, gbp
+
+
+def logsignature(path: torch.Tensor, depth: int, mode: str = "words", stream: bool = False,
+                 basepoint=None) -> torch.Tensor:
+    """LogSig^depth in the 'words' (default), 'brackets' or 'expand' basis."""
+    f, t = _bp_args(basepoint)
+    return _LogSignature.apply(path, depth, mode, stream, f, t)
+
+
+class _Combine(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, a, b, C, depth):
+        ctx.save_for_backward(a, b)
+        ctx.C, ctx.depth = C, depth
+        return sig_signature_combine(a, b, C, depth)
+
+    @staticmethod
+    def backward(ctx, g):
+        a, b = ctx.saved_tensors
+        ga, gb = sig_signature_combine_backward(g.contiguous(), a, b, ctx.C, ctx.depth)
+        return ga, gb, None, None
+
+
+def signature_combine(a: torch.Tensor, b: torch.Tensor, C: int, depth: int) -> torch.Tensor:
+    """a [x] b (Chen's identity), differentiable."""
+    return _Combine.apply(a, b, C, depth)
+
+
+def multi_signature_combine(sigs, C: int, depth: int) -> torch.Tensor:
+    """Ordered product of a list / [n, B, S] stack of signatures (forward only)."""
+    if isinstance(sigs, (list, tuple)):
+        sigs = torch.stack(list(sigs))
+    return sig_multi_signature_combine(sigs, C, depth)

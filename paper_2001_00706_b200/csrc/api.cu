@@ -1,0 +1,575 @@
+// api.cu -- the C ABI of libsig.so (include/sig.h): validation, kernel selection, launch plans.
+// No compute happens here: every step of the path runs in the sm_100a kernels of K1-K5.
+#include <atomic>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/sig.h"
+#include "combine.cuh"
+#include "logsig.cuh"
+#include "lyndon.h"
+#include "sig_bwd.cuh"
+#include "sig_table.h"
+
+using namespace sigb200;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+sig_status_t fail(sig_status_t st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+sig_status_t ok() {
+    g_last_error.clear();
+    return SIG_OK;
+}
+
+sig_status_t cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return ok();
+    return fail(SIG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int64_t sig_channels_checked(int64_t C, int32_t depth) {
+    if (C < 1 || depth < 1) return -1;
+    __int128 s = 0, p = 1;
+    for (int k = 1; k <= depth; ++k) {
+        p *= C;
+        s += p;
+        if (s > (__int128)INT64_MAX) return -1;
+    }
+    return (int64_t)s;
+}
+
+// ---------------------------------------------------------------- forward launch plan
+constexpr int64_t kTargetThreads = 148LL * 1024;  // ~2 resident waves of 512-thread CTAs
+constexpr int64_t kMinChunk = 64;                 // increments per time chunk, at least
+
+struct FwdPlan {
+    const KernelSet* ks;
+    int P;
+    FwdLaunch launch;
+    int64_t M, n_chunks, chunk_len;
+    int G;                  // group size of the chunk fold
+    int64_t fold_levels[40];
+    int n_fold;             // number of fold launches (after the scan)
+    size_t ws_bytes;
+};
+
+int group_size_for(int64_t S) {
+    int G = 32;
+    while (G > 2 && (size_t)G * S * sizeof(float) > 200 * 1024) G >>= 1;
+    if ((size_t)G * S * sizeof(float) > 200 * 1024) return 0;  // pairwise in global memory
+    return G;
+}
+
+void plan_fold(int64_t n, int64_t S, int64_t B, int& G, int64_t* lv, int& nl, size_t& elems) {
+    // n elements per path -> ... -> 1; intermediate results go to the workspace (the last to out)
+    G = group_size_for(S);
+    const int g = G > 0 ? G : 2;
+    nl = 0;
+    elems = 0;
+    while (n > 1) {
+        n = (n + g - 1) / g;
+        lv[nl++] = n;
+        if (n > 1) elems += (size_t)n * B * S;
+    }
+}
+
+sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
+                           FwdPlan& pl) {
+    if (C < 1 || depth < 1) return fail(SIG_ERR_INVALID_ARG, "C=%lld depth=%d must be >= 1", (long long)C, depth);
+    if (B < 0) return fail(SIG_ERR_SHAPE, "B=%lld < 0", (long long)B);
+    if (bp != SIG_BP_NONE && bp != SIG_BP_ZERO && bp != SIG_BP_GIVEN)
+        return fail(SIG_ERR_INVALID_ARG, "bad basepoint mode %d", (int)bp);
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0) return fail(SIG_ERR_SHAPE, "signature size overflows int64");
+    const int64_t M = L - 1 + (bp != SIG_BP_NONE ? 1 : 0);
+    if (M < 1)
+        return fail(SIG_ERR_SHAPE, "a stream needs >= 2 points (P:L69); got L=%lld%s", (long long)L,
+                    bp != SIG_BP_NONE ? " with a basepoint (L >= 1 needed)" : "");
+    const KernelSet* ks = (C <= 8) ? find_kernels((int)C, depth) : nullptr;
+    if (!ks) return fail(SIG_ERR_UNSUPPORTED, "no sm_100a kernel instantiated for C=%lld depth=%d", (long long)C, depth);
+    pl.ks = ks;
+    pl.M = M;
+    pl.P = ks->pf0;
+    pl.launch = ks->fwd0;
+    const int64_t cp0 = sigb200::ipow(C, ks->pf0);
+    pl.n_chunks = 1;
+    if (!stream && B > 0 && B * cp0 < kTargetThreads && M >= 2 * kMinChunk) {
+        int64_t want = (kTargetThreads + B * cp0 - 1) / (B * cp0);
+        int64_t maxc = M / kMinChunk;
+        pl.n_chunks = want < maxc ? want : maxc;
+    }
+    if (pl.n_chunks == 1 && B * cp0 < kTargetThreads && ks->fwd1) {
+        pl.P = ks->pf1;
+        pl.launch = ks->fwd1;
+    }
+    pl.chunk_len = (M + pl.n_chunks - 1) / pl.n_chunks;
+    pl.n_chunks = (M + pl.chunk_len - 1) / pl.chunk_len;
+    size_t elems = 0;
+    pl.n_fold = 0;
+    pl.G = 0;
+    if (pl.n_chunks > 1) {
+        plan_fold(pl.n_chunks, S, B, pl.G, pl.fold_levels, pl.n_fold, elems);
+        elems += (size_t)pl.n_chunks * B * S;  // the chunk signatures themselves
+    }
+    pl.ws_bytes = elems * sizeof(float);
+    return ok();
+}
+
+// fold n elements per path (element (j, b) at in + j*sj + b*sb) into out[b] (row stride S)
+cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_t sb, int64_t n, int64_t B, float* out,
+                        float* ws, cudaStream_t st) {
+    const int64_t S = d.S;
+    if (n == 1) {
+        return cudaMemcpy2DAsync(out, S * sizeof(float), in, sb * sizeof(float), S * sizeof(float), B,
+                                 cudaMemcpyDeviceToDevice, st);
+    }
+    int G = group_size_for(S);
+    const float* cur = in;
+    int64_t csj = sj, csb = sb;
+    float* buf = ws;
+    while (n > 1) {
+        const int g = G > 0 ? G : 2;
+        const int64_t ng = (n + g - 1) / g;
+        float* dst;
+        int64_t dsj, dsb;
+        if (ng == 1) {
+            dst = out;
+            dsj = 0;
+            dsb = S;
+        } else {
+            dst = buf;
+            dsj = B * S;  // [ng, B, S]
+            dsb = S;
+            buf += ng * B * S;
+        }
+        if (G > 0) {
+            GroupParams gp;
+            gp.d = d;
+            gp.in = cur;
+            gp.in_sj = csj;
+            gp.in_sb = csb;
+            gp.n = n;
+            gp.G = G;
+            gp.out = dst;
+            gp.out_sj = dsj;
+            gp.out_sb = dsb;
+            const size_t smem = (size_t)G * S * sizeof(float);
+            if (smem > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(combine_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)smem);
+                if (e != cudaSuccess) return e;
+            }
+            dim3 grid((unsigned)ng, (unsigned)B);
+            combine_group_kernel<<<grid, 256, smem, st>>>(gp);
+            count_launch();
+        } else {
+            // pairwise in global memory: dst(g) = cur(2g) [x] cur(2g+1)
+            for (int64_t q = 0; q < ng; ++q) {
+                const float* a = cur + 2 * q * csj;
+                float* o = dst + q * dsj;
+                if (2 * q + 1 < n) {
+                    dim3 grid((unsigned)((S + 255) / 256), (unsigned)B);
+                    combine_pair_kernel<<<grid, 256, 0, st>>>(d, a, csb, a + csj, csb, o, dsb);
+                    count_launch();
+                } else {
+                    cudaError_t e = cudaMemcpy2DAsync(o, dsb * sizeof(float), a, csb * sizeof(float),
+                                                      S * sizeof(float), B, cudaMemcpyDeviceToDevice, st);
+                    if (e != cudaSuccess) return e;
+                }
+            }
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        cur = dst;
+        csj = dsj;
+        csb = dsb;
+        n = ng;
+    }
+    return cudaSuccess;
+}
+
+sig_status_t run_signature(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                           sig_basepoint_t bp, const float* basepoint, float* out, void* ws, size_t ws_bytes,
+                           cudaStream_t s) {
+    FwdPlan pl;
+    sig_status_t st = make_fwd_plan(B, L, C, depth, stream, bp, pl);
+    if (st != SIG_OK) return st;
+    if (B == 0) return ok();  // empty batch: nothing to do (empty tensors may carry null pointers)
+    if (!path || !out) return fail(SIG_ERR_INVALID_ARG, "path and out must be non-null");
+    if (bp == SIG_BP_GIVEN && !basepoint) return fail(SIG_ERR_INVALID_ARG, "basepoint is NULL with SIG_BP_GIVEN");
+    if (ws_bytes < pl.ws_bytes || (pl.ws_bytes > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", pl.ws_bytes, ws_bytes);
+    const TensorDims d = make_dims((int)C, depth);
+    FwdParams prm{};
+    prm.path = path;
+    prm.basepoint = basepoint;
+    prm.bp_mode = (int)bp;
+    prm.stream = stream ? 1 : 0;
+    prm.B = B;
+    prm.L = L;
+    prm.M = pl.M;
+    prm.chunk_len = pl.chunk_len;
+    prm.n_chunks = pl.n_chunks;
+    prm.n_units = B * pl.n_chunks;
+    float* units = (pl.n_chunks > 1) ? static_cast<float*>(ws) : out;
+    prm.out = units;
+    cudaError_t e = pl.launch(prm, s);
+    if (e != cudaSuccess) return cuda_status(e, "signature scan launch");
+    count_launch();
+    if (pl.n_chunks > 1) {
+        // unit (b, j) at units + (b*n_chunks + j)*S  ->  element (j, b): sj = S, sb = n_chunks*S
+        float* fold_ws = units + (size_t)pl.n_chunks * B * d.S;
+        e = launch_fold(d, units, d.S, pl.n_chunks * d.S, pl.n_chunks, B, out, fold_ws, s);
+        if (e != cudaSuccess) return cuda_status(e, "chunk fold launch");
+    }
+    return ok();
+}
+
+// ---------------------------------------------------------------- logsig plans
+struct DeviceTables {
+    int64_t* lyn_idx = nullptr;
+    int *rowptr = nullptr, *col = nullptr, *rowptrT = nullptr, *colT = nullptr;
+    float *val = nullptr, *valT = nullptr;
+    int device = 0;
+};
+
+}  // namespace
+
+struct sig_logsig_plan_s {
+    int C, N;
+    sig_logsig_mode_t mode;
+    int64_t S, w;
+    DeviceTables dt;
+};
+
+namespace {
+
+template <class T>
+cudaError_t upload(T** dst, const std::vector<T>& v) {
+    *dst = nullptr;
+    if (v.empty()) return cudaSuccess;
+    cudaError_t e = cudaMalloc(dst, v.size() * sizeof(T));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+LogsigTables device_view(const sig_logsig_plan_s* pl) {
+    LogsigTables tb{};
+    tb.w = (int)pl->w;
+    tb.lyn_idx = pl->dt.lyn_idx;
+    tb.minv_rowptr = pl->dt.rowptr;
+    tb.minv_col = pl->dt.col;
+    tb.minv_val = pl->dt.val;
+    tb.minvT_rowptr = pl->dt.rowptrT;
+    tb.minvT_col = pl->dt.colT;
+    tb.minvT_val = pl->dt.valT;
+    return tb;
+}
+
+sig_status_t check_logsig_smem(const TensorDims& d, int64_t w) {
+    if (logsig_fwd_smem(d, (int)w) > 227 * 1024 || logsig_bwd_smem(d) > 227 * 1024)
+        return fail(SIG_ERR_UNSUPPORTED, "logsignature of C=%d depth=%d exceeds one CTA's shared memory", d.C, d.N);
+    return SIG_OK;
+}
+
+}  // namespace
+
+// ================================================================ extern "C"
+extern "C" {
+
+int64_t sig_signature_channels(int64_t C, int32_t depth) { return sig_channels_checked(C, depth); }
+
+int64_t sig_logsignature_channels(int64_t C, int32_t depth, sig_logsig_mode_t mode) {
+    if (C < 1 || depth < 1) return -1;
+    if (mode == SIG_LOGSIG_EXPAND) return sig_channels_checked(C, depth);
+    if (mode == SIG_LOGSIG_WORDS || mode == SIG_LOGSIG_BRACKETS) return witt_dimension(C, depth);
+    return -1;
+}
+
+int32_t sig_is_supported(int64_t C, int32_t depth, int32_t backward) {
+    if (C < 1 || C > 8 || depth < 1) return 0;
+    const KernelSet* ks = find_kernels((int)C, depth);
+    if (!ks) return 0;
+    return backward ? (ks->bwd != nullptr) : 1;
+}
+
+uint64_t sig_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* sig_status_string(sig_status_t st) {
+    switch (st) {
+        case SIG_OK: return "SIG_OK";
+        case SIG_ERR_INVALID_ARG: return "SIG_ERR_INVALID_ARG";
+        case SIG_ERR_SHAPE: return "SIG_ERR_SHAPE";
+        case SIG_ERR_UNSUPPORTED: return "SIG_ERR_UNSUPPORTED";
+        case SIG_ERR_CUDA: return "SIG_ERR_CUDA";
+        case SIG_ERR_WORKSPACE: return "SIG_ERR_WORKSPACE";
+    }
+    return "SIG_ERR_UNKNOWN";
+}
+
+const char* sig_last_error(void) { return g_last_error.c_str(); }
+
+size_t sig_signature_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                                    sig_basepoint_t bp) {
+    FwdPlan pl;
+    if (make_fwd_plan(B, L, C, depth, stream, bp, pl) != SIG_OK) return 0;
+    return pl.ws_bytes;
+}
+
+sig_status_t sig_signature(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                           sig_basepoint_t bp, const float* basepoint, float* out, void* ws, size_t ws_bytes,
+                           sig_cuda_stream_t s) {
+    return run_signature(path, B, L, C, depth, stream, bp, basepoint, out, ws, ws_bytes, (cudaStream_t)s);
+}
+
+sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
+                                    int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
+                                    const float* basepoint, float* grad_path, float* grad_basepoint,
+                                    sig_cuda_stream_t s) {
+    FwdPlan pl;
+    sig_status_t st = make_fwd_plan(B, L, C, depth, stream, bp, pl);
+    if (st != SIG_OK) return st;
+    if (!pl.ks->bwd)
+        return fail(SIG_ERR_UNSUPPORTED, "no sm_100a backward kernel for C=%lld depth=%d", (long long)C, depth);
+    if (B == 0) return ok();
+    if (!grad_out || !path || !out_saved || !grad_path)
+        return fail(SIG_ERR_INVALID_ARG, "grad_out, path, out_saved and grad_path must be non-null");
+    if (bp == SIG_BP_GIVEN && !basepoint) return fail(SIG_ERR_INVALID_ARG, "basepoint is NULL with SIG_BP_GIVEN");
+    BwdParams prm{};
+    prm.grad_out = grad_out;
+    prm.path = path;
+    prm.basepoint = basepoint;
+    prm.sig_final = out_saved;
+    prm.bp_mode = (int)bp;
+    prm.stream = stream ? 1 : 0;
+    prm.B = B;
+    prm.L = L;
+    prm.M = pl.M;
+    prm.grad_path = grad_path;
+    prm.grad_bp = (bp == SIG_BP_GIVEN) ? grad_basepoint : nullptr;
+    cudaError_t e = pl.ks->bwd(prm, (cudaStream_t)s);
+    if (e == cudaSuccess) count_launch();
+    if (e == cudaErrorInvalidConfiguration)
+        return fail(SIG_ERR_UNSUPPORTED, "path of %lld increments does not fit the backward's shared memory",
+                    (long long)pl.M);
+    return cuda_status(e, "signature backward launch");
+}
+
+sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, int64_t C, int32_t depth, float* out,
+                                   sig_cuda_stream_t s) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || depth > 15) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (!a || !b || !out) return fail(SIG_ERR_INVALID_ARG, "a, b and out must be non-null");
+    if (B < 0) return fail(SIG_ERR_SHAPE, "B < 0");
+    if (B == 0) return ok();
+    const TensorDims d = make_dims((int)C, depth);
+    dim3 grid((unsigned)((S + 255) / 256), (unsigned)B);
+    combine_pair_kernel<<<grid, 256, 0, (cudaStream_t)s>>>(d, a, S, b, S, out, S);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "combine launch");
+}
+
+sig_status_t sig_signature_combine_backward(const float* grad_out, const float* a, const float* b, int64_t B,
+                                            int64_t C, int32_t depth, float* grad_a, float* grad_b,
+                                            sig_cuda_stream_t s) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || depth > 15) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (!grad_out || !a || !b) return fail(SIG_ERR_INVALID_ARG, "grad_out, a and b must be non-null");
+    if (B < 0) return fail(SIG_ERR_SHAPE, "B < 0");
+    if (B == 0 || (!grad_a && !grad_b)) return ok();
+    const TensorDims d = make_dims((int)C, depth);
+    dim3 grid((unsigned)((S + 255) / 256), (unsigned)B);
+    combine_pair_bwd_kernel<<<grid, 256, 0, (cudaStream_t)s>>>(d, grad_out, a, b, grad_a, grad_b);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "combine backward launch");
+}
+
+size_t sig_multi_signature_combine_workspace_size(int64_t n, int64_t B, int64_t C, int32_t depth) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || n < 1 || B < 0) return 0;
+    int G;
+    int64_t lv[64];
+    int nl;
+    size_t elems;
+    plan_fold(n, S, B, G, lv, nl, elems);
+    return elems * sizeof(float);
+}
+
+sig_status_t sig_multi_signature_combine(const float* sigs, int64_t n, int64_t B, int64_t C, int32_t depth,
+                                         float* out, void* ws, size_t ws_bytes, sig_cuda_stream_t s) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || depth > 15) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (!sigs || !out) return fail(SIG_ERR_INVALID_ARG, "sigs and out must be non-null");
+    if (n < 1 || B < 0) return fail(SIG_ERR_SHAPE, "n=%lld must be >= 1", (long long)n);
+    const size_t need = sig_multi_signature_combine_workspace_size(n, B, C, depth);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    if (B == 0) return ok();
+    const TensorDims d = make_dims((int)C, depth);
+    cudaError_t e = launch_fold(d, sigs, B * S, S, n, B, out, static_cast<float*>(ws), (cudaStream_t)s);
+    return cuda_status(e, "multi combine launch");
+}
+
+sig_status_t sig_logsig_plan_create(int64_t C, int32_t depth, sig_logsig_mode_t mode, sig_logsig_plan_t* plan) {
+    if (!plan) return fail(SIG_ERR_INVALID_ARG, "plan is NULL");
+    *plan = nullptr;
+    if (C < 1 || C > 8 || depth < 1 || depth > 15)
+        return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (mode != SIG_LOGSIG_EXPAND && mode != SIG_LOGSIG_BRACKETS && mode != SIG_LOGSIG_WORDS)
+        return fail(SIG_ERR_INVALID_ARG, "bad logsignature mode %d", (int)mode);
+    if (!find_kernels((int)C, depth))
+        return fail(SIG_ERR_UNSUPPORTED, "no sm_100a kernel instantiated for C=%lld depth=%d", (long long)C, depth);
+    const TensorDims d = make_dims((int)C, depth);
+    auto pl = std::make_unique<sig_logsig_plan_s>();
+    pl->C = (int)C;
+    pl->N = depth;
+    pl->mode = mode;
+    pl->S = d.S;
+    pl->w = (mode == SIG_LOGSIG_EXPAND) ? d.S : witt_dimension(C, depth);
+    sig_status_t st = check_logsig_smem(d, pl->w);
+    if (st != SIG_OK) return st;
+    cudaGetDevice(&pl->dt.device);
+    if (mode != SIG_LOGSIG_EXPAND) {
+        LyndonTables T;
+        try {
+            T = build_lyndon_tables((int)C, depth, mode == SIG_LOGSIG_BRACKETS);
+        } catch (const std::exception& ex) {
+            return fail(SIG_ERR_INVALID_ARG, "Lyndon tables: %s", ex.what());
+        }
+        if ((int64_t)T.flat_index.size() != pl->w)
+            return fail(SIG_ERR_INVALID_ARG, "Lyndon word count %zu != Witt %lld", T.flat_index.size(),
+                        (long long)pl->w);
+        std::vector<float> v(T.minv_val.begin(), T.minv_val.end()), vT(T.minvT_val.begin(), T.minvT_val.end());
+        cudaError_t e = upload(&pl->dt.lyn_idx, T.flat_index);
+        if (e == cudaSuccess) e = upload(&pl->dt.rowptr, T.minv_rowptr);
+        if (e == cudaSuccess) e = upload(&pl->dt.col, T.minv_col);
+        if (e == cudaSuccess) e = upload(&pl->dt.val, v);
+        if (e == cudaSuccess) e = upload(&pl->dt.rowptrT, T.minvT_rowptr);
+        if (e == cudaSuccess) e = upload(&pl->dt.colT, T.minvT_col);
+        if (e == cudaSuccess) e = upload(&pl->dt.valT, vT);
+        if (e != cudaSuccess) {
+            sig_logsig_plan_destroy(pl.release());
+            return cuda_status(e, "logsig plan upload");
+        }
+    }
+    *plan = pl.release();
+    return ok();
+}
+
+sig_status_t sig_logsig_plan_destroy(sig_logsig_plan_t plan) {
+    if (!plan) return ok();
+    cudaFree(plan->dt.lyn_idx);
+    cudaFree(plan->dt.rowptr);
+    cudaFree(plan->dt.col);
+    cudaFree(plan->dt.val);
+    cudaFree(plan->dt.rowptrT);
+    cudaFree(plan->dt.colT);
+    cudaFree(plan->dt.valT);
+    delete plan;
+    return ok();
+}
+
+size_t sig_logsignature_workspace_size(sig_logsig_plan_t plan, int64_t B, int64_t L, int32_t stream,
+                                       sig_basepoint_t bp) {
+    if (!plan) return 0;
+    FwdPlan pl;
+    if (make_fwd_plan(B, L, plan->C, plan->N, stream, bp, pl) != SIG_OK) return 0;
+    const int64_t rows = stream ? B * pl.M : B;
+    // scan workspace | signature (if the caller gives no sig_saved) | dense dL/dlog and dL/dSig
+    size_t a = pl.ws_bytes;
+    size_t b = (size_t)rows * plan->S * sizeof(float) * 3;
+    return a + b;
+}
+
+sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t B, int64_t L, int32_t stream,
+                              sig_basepoint_t bp, const float* basepoint, float* out, float* sig_saved, void* ws,
+                              size_t ws_bytes, sig_cuda_stream_t s) {
+    if (!plan) return fail(SIG_ERR_INVALID_ARG, "plan is NULL");
+    if (!out) return fail(SIG_ERR_INVALID_ARG, "out is NULL");
+    FwdPlan pl;
+    sig_status_t st = make_fwd_plan(B, L, plan->C, plan->N, stream, bp, pl);
+    if (st != SIG_OK) return st;
+    const size_t need = sig_logsignature_workspace_size(plan, B, L, stream, bp);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    if (B == 0) return ok();
+    const int64_t rows = stream ? B * pl.M : B;
+    char* wsb = static_cast<char*>(ws);
+    float* sig = sig_saved ? sig_saved : reinterpret_cast<float*>(wsb + pl.ws_bytes);
+    st = run_signature(path, B, L, plan->C, plan->N, stream, bp, basepoint, sig, ws, pl.ws_bytes, (cudaStream_t)s);
+    if (st != SIG_OK) return st;
+    LogsigParams p{};
+    p.d = make_dims(plan->C, plan->N);
+    p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
+    p.tb = device_view(plan);
+    p.rows = rows;
+    p.sig = sig;
+    p.out = out;
+    const size_t smem = logsig_fwd_smem(p.d, (int)plan->w);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(logsig_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_status(e, "logsig smem attribute");
+    }
+    logsig_fwd_kernel<<<(unsigned)rows, 256, smem, (cudaStream_t)s>>>(p);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "logsig launch");
+}
+
+sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad_out, const float* path,
+                                       const float* sig_saved, int64_t B, int64_t L, int32_t stream,
+                                       sig_basepoint_t bp, const float* basepoint, float* grad_path,
+                                       float* grad_basepoint, void* ws, size_t ws_bytes, sig_cuda_stream_t s) {
+    if (!plan) return fail(SIG_ERR_INVALID_ARG, "plan is NULL");
+    if (!grad_out || !path || !sig_saved || !grad_path)
+        return fail(SIG_ERR_INVALID_ARG, "grad_out, path, sig_saved and grad_path must be non-null");
+    FwdPlan pl;
+    sig_status_t st = make_fwd_plan(B, L, plan->C, plan->N, stream, bp, pl);
+    if (st != SIG_OK) return st;
+    if (!pl.ks->bwd)
+        return fail(SIG_ERR_UNSUPPORTED, "no sm_100a backward kernel for C=%d depth=%d", plan->C, plan->N);
+    const size_t need = sig_logsignature_workspace_size(plan, B, L, stream, bp);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    if (B == 0) return ok();
+    const int64_t rows = stream ? B * pl.M : B;
+    char* wsb = static_cast<char*>(ws) + pl.ws_bytes;
+    float* glog = reinterpret_cast<float*>(wsb) + (size_t)rows * plan->S;
+    float* gsig = glog + (size_t)rows * plan->S;
+    LogsigParams p{};
+    p.d = make_dims(plan->C, plan->N);
+    p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
+    p.tb = device_view(plan);
+    p.rows = rows;
+    p.sig = sig_saved;
+    p.gout = grad_out;
+    p.gsig = gsig;
+    p.glog_ws = glog;
+    const size_t smem = logsig_bwd_smem(p.d);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(logsig_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
+    }
+    logsig_bwd_kernel<<<(unsigned)rows, 256, smem, (cudaStream_t)s>>>(p);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");
+    return sig_signature_backward(gsig, path, sig_saved, B, L, plan->C, plan->N, stream, bp, basepoint, grad_path,
+                                  grad_basepoint, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// combine.cuh -- K3: the group-like product [x] on batches of signatures, sm_100a.
+//
+//   (A [x] B)_k = sum_{i=0}^{k} A_i (x) B_{k-i},  A_0 = B_0 = 1     (eq-tensorproduct)
+//
+// Used for signature_combine / multi_signature_combine and to fold the signatures
+// of time chunks in order (Chen's identity eq-grouplike; "parallelised in the usual way
+// for reductions").  One thread computes one output coefficient: word w at level k costs
+// k-1 FMAs, A_i[w / C^(k-i)] * B_{k-i}[w mod C^(k-i)].  The work is small and HBM/L2-bound, so
+// C and N are runtime values here (no template explosion).
+//
+// Group fold: a CTA loads G consecutive signatures of one path into shared memory and reduces
+// them with an ordered binary tree (time order is preserved: [x] is associative but not
+// commutative).  In-place update of the left operand is safe level by level, top-down: level k
+// reads only levels < k of the left operand and its own coefficient.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sigb200 {
+
+struct TensorDims {
+    int C, N;
+    int64_t S;
+    int64_t off[17];   // off[k] = flat offset of level k (1-based), off[N+1] = S
+    int64_t pw[17];    // pw[k] = C^k
+};
+
+inline TensorDims make_dims(int C, int N) {
+    TensorDims d{};
+    d.C = C;
+    d.N = N;
+    d.pw[0] = 1;
+    for (int k = 1; k <= 16; ++k) d.pw[k] = (k <= N + 1) ? d.pw[k - 1] * C : 0;
+    d.off[1] = 0;
+    for (int k = 1; k <= N; ++k) d.off[k + 1] = d.off[k] + d.pw[k];
+    d.S = d.off[N + 1];
+    return d;
+}
+
+__device__ __forceinline__ int level_of(const TensorDims& d, int64_t f) {
+    int k = 1;
+    while (k < d.N && f >= d.off[k + 1]) ++k;
+    return k;
+}
+
+// out = a [x] b for one flat coefficient f (level k, word w)
+__device__ __forceinline__ float mul_coef(const TensorDims& d, const float* a, const float* b, int k, int64_t w) {
+    float acc = a[d.off[k] + w] + b[d.off[k] + w];
+    for (int i = 1; i < k; ++i) {
+        const int64_t q = d.pw[k - i];
+        acc = fmaf(a[d.off[i] + w / q], b[d.off[k - i] + w % q], acc);
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------- pairwise, batched
+// row r: out + r*so = (a + r*sa) [x] (b + r*sb)
+__global__ void combine_pair_kernel(const TensorDims d, const float* __restrict__ a, int64_t sa,
+                                    const float* __restrict__ b, int64_t sb, float* __restrict__ out, int64_t so) {
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (f >= d.S) return;
+    const int k = level_of(d, f);
+    out[r * so + f] = mul_coef(d, a + r * sa, b + r * sb, k, f - d.off[k]);
+}
+
+// ---------------------------------------------------------------- VJP of a [x] b
+//   ga_i[u] = go_i[u] + sum_{k>i} sum_v go_k[u v] b_{k-i}[v]
+//   gb_j[v] = go_j[v] + sum_{k>j} sum_u go_k[u v] a_{k-j}[u]
+__global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restrict__ go, const float* __restrict__ a,
+                                        const float* __restrict__ b, float* __restrict__ ga, float* __restrict__ gb) {
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (f >= d.S) return;
+    const int i = level_of(d, f);
+    const int64_t u = f - d.off[i];
+    const float* gor = go + r * d.S;
+    const float* ar = a + r * d.S;
+    const float* br = b + r * d.S;
+    if (ga) {
+        float acc = gor[f];
+        for (int k = i + 1; k <= d.N; ++k) {
+            const int64_t nv = d.pw[k - i];
+            const float* gk = gor + d.off[k] + u * nv;
+            const float* bk = br + d.off[k - i];
+            for (int64_t v = 0; v < nv; ++v) acc = fmaf(gk[v], bk[v], acc);
+        }
+        ga[r * d.S + f] = acc;
+    }
+    if (gb) {
+        // f indexes level j = i, word v = u
+        float acc = gor[f];
+        for (int k = i + 1; k <= d.N; ++k) {
+            const int64_t nu = d.pw[k - i];
+            const int64_t stride = d.pw[i];
+            const float* gk = gor + d.off[k] + u;
+            const float* ak = ar + d.off[k - i];
+            for (int64_t uu = 0; uu < nu; ++uu) acc = fmaf(gk[uu * stride], ak[uu], acc);
+        }
+        gb[r * d.S + f] = acc;
+    }
+}
+
+// ---------------------------------------------------------------- ordered group fold in smem
+struct GroupParams {
+    TensorDims d;
+    const float* in;
+    int64_t in_sj, in_sb;    // element (j, b) at in + j*in_sj + b*in_sb
+    int64_t n;               // elements per path
+    int G;                   // group size (power of two)
+    float* out;
+    int64_t out_sj, out_sb;  // group result (g, b) at out + g*out_sj + b*out_sb
+};
+
+__global__ void combine_group_kernel(const GroupParams p) {
+    extern __shared__ float gs[];  // [G][S]
+    const TensorDims& d = p.d;
+    const int64_t g = blockIdx.x, b = blockIdx.y;
+    const int64_t j0 = g * p.G;
+    const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
+    const int64_t S = d.S;
+    for (int64_t e = threadIdx.x; e < (int64_t)cnt * S; e += blockDim.x) {
+        const int64_t jj = e / S, f = e % S;
+        gs[e] = p.in[(j0 + jj) * p.in_sj + b * p.in_sb + f];
+    }
+    __syncthreads();
+    for (int stride = 1; stride < cnt; stride <<= 1) {
+        const int npairs = (cnt + 2 * stride - 1) / (2 * stride);
+        for (int k = d.N; k >= 1; --k) {
+            const int64_t nw = d.pw[k];
+            for (int64_t e = threadIdx.x; e < (int64_t)npairs * nw; e += blockDim.x) {
+                const int pr = (int)(e / nw);
+                const int64_t w = e % nw;
+                const int left = pr * 2 * stride, right = left + stride;
+                if (right >= cnt) continue;
+                float* x = gs + (int64_t)left * S;
+                const float* y = gs + (int64_t)right * S;
+                x[d.off[k] + w] = mul_coef(d, x, y, k, w);
+            }
+            __syncthreads();
+        }
+    }
+    float* o = p.out + g * p.out_sj + b * p.out_sb;
+    for (int64_t f = threadIdx.x; f < S; f += blockDim.x) o[f] = gs[f];
+}
+
+}  // namespace sigb200

@@ -1,0 +1,356 @@
+// sig_bwd.cuh -- K2: reversible backward of the signature, sm_100a.
+//
+// Method: Appendix C.  Walking t = M-1 .. 0 with the state A' = Sig after step t:
+//   (1) reversibility (eq-reverse): A = A' [x] exp(-z_t), the same fused Horner update
+//       with the increment negated.  Only levels < N are rebuilt: the VJP never reads A_N.
+//   (2) recompute the Horner chains of eq-fusedterm from A:
+//       B^(k)_0 = 1,  B^(k)_i = B^(k)_{i-1} (x) z/(k-i+1) + A_i.
+//   (3) VJP of the chains, k = 1..N bottom-up so the incoming gradient G'_k is read before any
+//       chain k' > k adds into it:  beta <- G'_k;  for i = k..1 (s = k-i+1):
+//         gz[c] += (1/s) sum_w B_{i-1}[w] beta[w c];   beta <- (1/s) sum_c beta[. c] z_c;
+//         G_{i-1} += beta  (i >= 2)
+//   (4) grad x_{t+1} += gz, grad x_t -= gz.
+// The top-level gradient G_N is never modified (it is constant over all steps).
+//
+// B200 design: one CTA per path, one thread per word prefix p of length P.
+// * Levels >= P: the thread holds G and A for the words starting with p in registers and runs
+//   (1)-(3) on them depth-first with no communication (as in the forward).
+// * Levels < P: every operation there is LINEAR in the gradient.  So instead of reducing the
+//   chain values beta_P[p] over threads every step, thread p keeps its own partial of the
+//   low-level gradient, Ghat_i(p) with G_i[u] = sum_{p : p[:i] = u} Ghat_i(p), and runs the low
+//   tails of all chains along its own prefix (it already holds the prefix chain values B_i[p[:i]]).
+//   Its contributions to gz at level i land in channel p_{i-1}.  Grad-out coefficients of the low
+//   levels are owned by the thread whose trailing prefix digits are zero.
+// * The only collective per step is the C-vector gz: one warp reduce-scatter (channel = lane mod
+//   C when C divides 32, which also absorbs the per-level scalars), then one float per warp and
+//   channel into a shared-memory tile; every T steps the CTA sums the tile in a fixed order and
+//   writes the gradient rows.  No cross-warp synchronisation inside a tile.
+// All reductions have a fixed order, so results are bitwise reproducible.
+#pragma once
+#include "sig_fwd.cuh"
+
+namespace sigb200 {
+
+struct BwdParams {
+    const float* grad_out;   // [B, S] | stream: [B, M, S]
+    const float* path;       // [B, L, C]
+    const float* basepoint;  // [B, C] (bp_mode == 2)
+    const float* sig_final;  // forward output: [B, S] | stream: [B, M, S]
+    int bp_mode, stream;
+    int64_t B, L, M;
+    float* grad_path;        // [B, L, C]
+    float* grad_bp;          // [B, C] or nullptr
+};
+
+template <class SH>
+struct BwdLayout {
+    static constexpr int C = SH::C, N = SH::N, P = SH::P;
+    static constexpr int HW = (SH::CP + 31) / 32;  // warps
+    static constexpr int NT = HW * 32;
+    // warp-shuffle reduction applies when C is a power of two dividing 32 and the warps are full
+    static constexpr bool FAST = (32 % C == 0) && ((C & (C - 1)) == 0) && (SH::CP % 32 == 0);
+    static constexpr int PL = P > 0 ? P : 1;
+    static constexpr int REC = FAST ? C : (C + PL);  // floats per record
+    static constexpr int RECS = FAST ? HW : NT;      // records per step
+    __host__ __device__ static int tile(int64_t M) {
+        int T = 32;
+        while (T > 1 && (size_t)T * RECS * REC * sizeof(float) > 64 * 1024) T >>= 1;
+        return (int)(T < M ? T : M);
+    }
+    static size_t smem_bytes(int64_t M) {
+        const size_t zf = (size_t)((M * C + 3) / 4 * 4);
+        const size_t T = (size_t)tile(M);
+        return (zf + T * RECS * REC + T * C + 32) * sizeof(float);
+    }
+};
+
+// VJP of the level-K Horner chain, depth-first over the thread's word tree (post-order).
+// Node (I, W) with chain value BI = B_I[p.W] returns beta_I[p.W] = (1/s) sum_c beta_{I+1}[p.W.c] z_c
+// (s = K-I), after adding the level-(I+1) gz contributions (1/s) B_I[p.W] beta_{I+1}[p.W.c] and
+// G_I += beta_I for owned levels I < K.  The leaves are beta_K = G_K (read before any chain
+// k' > K adds into it: chains run bottom-up).
+template <class SH, int K, int I, int W, int SA>
+__device__ __forceinline__ float vjp_visit(float BI, float (&G)[SH::OWN], const float (&A)[SA], const float (&z)[SH::C],
+                                           float (&gz)[SH::C]) {
+    constexpr int C = SH::C;
+    constexpr float sc = inv_int(K - I);
+    const float bs = BI * sc;
+    float acc = 0.0f;
+    static_for<0, C>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        constexpr int child = W * C + c;
+        float x;
+        if constexpr (I + 1 == K) {
+            x = G[SH::own_off(K) + child];
+        } else {
+            const float Bc = fmaf(bs, z[c], A[SH::own_off(I + 1) + child]);
+            x = vjp_visit<SH, K, I + 1, child>(Bc, G, A, z, gz);
+        }
+        gz[c] = fmaf(bs, x, gz[c]);
+        acc = fmaf(x, z[c], acc);
+    });
+    const float beta = acc * sc;
+    if constexpr (I >= SH::K0) G[SH::own_off(I) + W] += beta;
+    return beta;
+}
+
+// Prefix chain of chain K: Bp[j] = B^(K)_j[p[:j]] for j = 1..min(K-1, P) (Bp[0] = 1).
+template <class SH, int K, int SA>
+__device__ __forceinline__ void prefix_chain_all(float (&Bp)[SH::PL1], const float (&A)[SA], const float (&low)[SH::LOWA],
+                                                 const float (&zp)[SH::PD]) {
+    constexpr int P = SH::P;
+    constexpr int J = (K - 1 < P) ? K - 1 : P;
+    Bp[0] = 1.0f;
+    static_for<1, J + 1>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        float Aj;
+        if constexpr (j < P) Aj = low[j];
+        else Aj = A[SH::own_off(P)];
+        if constexpr (j == 1) Bp[j] = fmaf(zp[0], inv_int(K), Aj);
+        else Bp[j] = fmaf(Bp[j - 1] * inv_int(K - j + 1), zp[j - 1], Aj);
+    });
+}
+
+// Low tail of chain K from level I0 (<= P) down to 1 along the thread's prefix, on the partial
+// b = beta_{I0}(p): level-i gz contributions go to acc[i] (channel p_{i-1}); partials of
+// beta_{i-1} are added to Gh[i-1].
+template <class SH, int K, int I0>
+__device__ __forceinline__ void low_tail(float b, const float (&Bp)[SH::PL1], const float (&zp)[SH::PD],
+                                         float (&acc)[SH::PL1], float (&Gh)[SH::LOWA]) {
+    static_for<0, I0>([&](auto iic) {
+        constexpr int i = I0 - decltype(iic)::value;  // I0 .. 1
+        constexpr float sc = inv_int(K - i + 1);
+        acc[i] = fmaf(Bp[i - 1] * sc, b, acc[i]);
+        if constexpr (i >= 2) {
+            b = b * zp[i - 1] * sc;
+            Gh[i - 1] += b;
+        }
+    });
+}
+
+// STREAM (a template flag so that the plain kernel carries no stream-mode register pressure):
+// the gradient w.r.t. every prefix signature, grad_out[t], is added before step t is reversed.
+template <class SH, bool STREAM>
+__global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const BwdParams prm) {
+    using LY = BwdLayout<SH>;
+    constexpr int C = SH::C, N = SH::N, P = SH::P;
+    constexpr int HW = LY::HW;
+    constexpr int64_t S = SH::S;
+    extern __shared__ __align__(16) float sm[];
+    const int64_t M = prm.M;
+    const int64_t bidx = blockIdx.x;
+    const int T = LY::tile(M);
+    float* zbuf = sm;                                       // [M][C] increments
+    float* part = zbuf + (M * C + 3) / 4 * 4;               // [T][RECS][REC] per-step partials
+    float* tot = part + (size_t)T * LY::RECS * LY::REC;     // [T][C] per-step gz totals
+    float* gprev = tot + (size_t)T * C;                     // [C] gz of the step processed before
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int has_bp = prm.bp_mode != 0;
+    const float* sigrow = prm.sig_final + (STREAM ? ((size_t)bidx * M + (M - 1)) * S : (size_t)bidx * S);
+
+    for (int64_t e = tid; e < M * C; e += blockDim.x) {
+        const int64_t s = e / C;
+        const int c = (int)(e % C);
+        const float* xr = prm.path + bidx * prm.L * C;
+        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
+        const float x1 = xr[r1 * C + c];
+        const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
+        zbuf[e] = x1 - x0;
+    }
+    if (tid < C) gprev[tid] = 0.0f;
+
+    const bool valid = tid < SH::CP;
+    const int prefix = valid ? tid : 0;
+    int p[SH::PD];
+    prefix_digits<SH>(prefix, p);
+    float A[SH::OWNA];     // owned levels K0..N-1 of the current state
+    float G[SH::OWN];      // owned levels K0..N of the gradient
+    float low[SH::LOWA];   // A_i[p[:i]], i < P
+    float Gh[SH::LOWA];    // partial low-level gradients Ghat_i(p), i < P
+    static_for<SH::K0, N>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        load_run<SH::own(k), SH::own_off(k)>(A, sigrow + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
+    });
+    static_for<SH::K0, N + 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        if (STREAM || !valid) {
+#pragma unroll
+            for (int q = 0; q < SH::own(k); ++q) G[SH::own_off(k) + q] = 0.0f;
+        } else {
+            load_run<SH::own(k), SH::own_off(k)>(G, prm.grad_out + (size_t)bidx * S + SH::lvl_off(k) +
+                                                        (int64_t)prefix * SH::own(k));
+        }
+    });
+    low[0] = 0.0f;
+    Gh[0] = 0.0f;
+    // the low-level gradient coefficient u = p[:i] is owned by the thread with p[i:] == 0
+    static_for<1, P>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        constexpr int tail = (int)ipow(C, P - i);
+        low[i] = sigrow[SH::lvl_off(i) + prefix / tail];
+        Gh[i] = (!STREAM && valid && prefix % tail == 0)
+                    ? prm.grad_out[(size_t)bidx * S + SH::lvl_off(i) + prefix / tail]
+                    : 0.0f;
+    });
+    __syncthreads();
+
+    auto grad_row = [&](int64_t r) -> float* {
+        // augmented point r (r == 0 is the basepoint when one is given)
+        if (has_bp) {
+            if (r == 0) return (prm.bp_mode == 2 && prm.grad_bp) ? prm.grad_bp + bidx * C : nullptr;
+            return prm.grad_path + (bidx * prm.L + (r - 1)) * C;
+        }
+        return prm.grad_path + (bidx * prm.L + r) * C;
+    };
+
+    for (int64_t n0 = 0; n0 < M; n0 += T) {
+        const int tn = (int)((M - n0) < T ? (M - n0) : T);
+        for (int j = 0; j < tn; ++j) {
+            const int64_t t = M - 1 - (n0 + j);
+            if (STREAM && valid) {
+                const float* gr = prm.grad_out + ((size_t)bidx * M + t) * S;
+                static_for<SH::K0, N + 1>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    add_run<SH::own(k), SH::own_off(k)>(G, gr + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
+                });
+                static_for<1, P>([&](auto ic) {
+                    constexpr int i = decltype(ic)::value;
+                    constexpr int tail = (int)ipow(C, P - i);
+                    if (prefix % tail == 0) Gh[i] += gr[SH::lvl_off(i) + prefix / tail];
+                });
+            }
+            float z[C], zp[SH::PD];
+#pragma unroll
+            for (int c = 0; c < C; ++c) z[c] = zbuf[t * C + c];
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zp[q] = (P > 0) ? zbuf[t * C + p[q]] : 0.0f;
+
+            // (1) reversibility: A <- A [x] exp(-z) on levels < N; the exact identity at t = 0
+            if (t > 0) {
+                fused_mulexp<SH, N - 1, true>(A, low, z, zp);
+            } else {
+#pragma unroll
+                for (int q = 0; q < SH::OWNA; ++q) A[q] = 0.0f;
+#pragma unroll
+                for (int q = 0; q < SH::LOWA; ++q) low[q] = 0.0f;
+            }
+
+            // (2)+(3): chains k = 1..N bottom-up
+            float gz[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) gz[c] = 0.0f;
+            float acc[SH::PL1];
+#pragma unroll
+            for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
+            // chains entirely below P: read Ghat_k, tail from level k
+            static_for<1, P>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                float Bp[SH::PL1];
+                prefix_chain_all<SH, k>(Bp, A, low, zp);
+                low_tail<SH, k, k>(Gh[k], Bp, zp, acc, Gh);
+            });
+            // chains k >= max(P,1): owned levels depth-first, then the low tail from level P
+            static_for<SH::K0, N + 1>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                float Bp[SH::PL1];
+                prefix_chain_all<SH, k>(Bp, A, low, zp);
+                float bP;
+                if constexpr (k == P) bP = G[SH::own_off(P)];
+                else bP = vjp_visit<SH, k, P, 0>(Bp[P], G, A, z, gz);
+                if constexpr (P >= 1) low_tail<SH, k, P>(bP, Bp, zp, acc, Gh);
+            });
+
+            // ---- per-step gz: warp reduction into the tile
+            float* rec = part + (size_t)j * LY::RECS * LY::REC;
+            if constexpr (LY::FAST) {
+                // reduce-scatter over lane bits C/2 .. 1: lane l ends with channel l % C summed
+                // over its group of C lanes
+                float v[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) v[c] = gz[c];
+                static_for<0, ilog2(C)>([&](auto sc_) {
+                    constexpr int m = C >> (decltype(sc_)::value + 1);  // C/2, C/4, .., 1
+                    const bool up = (lane & m) != 0;
+#pragma unroll
+                    for (int q = 0; q < m; ++q) {
+                        const float send = up ? v[q] : v[q + m];
+                        const float keep = up ? v[q + m] : v[q];
+                        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                    }
+                });
+                float tv = v[0];
+                if constexpr (P >= 1) tv += acc[P];  // its channel p_{P-1} is lane % C
+                static_for<1, P>([&](auto ic) {
+                    constexpr int i = decltype(ic)::value;  // channel p_{i-1}: constant over the group
+                    float gsum = acc[i];
+#pragma unroll
+                    for (int m = 1; m < C; m <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, m);
+                    if ((lane % C) == p[i - 1]) tv += gsum;
+                });
+#pragma unroll
+                for (int m = C; m < 32; m <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, m);
+                if (lane < C) rec[warp * C + lane] = tv;
+            } else {
+                float* r = rec + (size_t)tid * LY::REC;
+#pragma unroll
+                for (int c = 0; c < C; ++c) r[c] = valid ? gz[c] : 0.0f;
+#pragma unroll
+                for (int q = 0; q < LY::PL; ++q) r[C + q] = (valid && P > 0) ? acc[q + 1] : 0.0f;
+            }
+        }
+        // ---- flush: per-step totals in a fixed order, then the gradient rows
+        __syncthreads();
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            const float* rec = part + (size_t)j * LY::RECS * LY::REC;
+            float s = 0.0f;
+            if constexpr (LY::FAST) {
+                for (int w = 0; w < HW; ++w) s += rec[w * C + c];
+            } else {
+                for (int th = 0; th < SH::CP; ++th) {
+                    const float* r = rec + (size_t)th * LY::REC;
+                    s += r[c];
+                    int q = th;
+                    for (int i = P; i >= 1; --i) {  // r[C + i - 1] belongs to channel p_{i-1}(th)
+                        if (q % C == c) s += r[C + i - 1];
+                        q /= C;
+                    }
+                }
+            }
+            tot[j * C + c] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            const int64_t t = M - 1 - (n0 + j);
+            const float before = (j == 0) ? gprev[c] : tot[(j - 1) * C + c];
+            float* gr = grad_row(t + 1);
+            if (gr) gr[c] = tot[j * C + c] - before;  // grad x_{t+1} = gz_t - gz_{t+1}
+            if (t == 0) {
+                float* g0 = grad_row(0);
+                if (g0) g0[c] = -tot[j * C + c];
+            }
+        }
+        __syncthreads();
+        if (tid < C) gprev[tid] = tot[(tn - 1) * C + tid];
+        __syncthreads();
+    }
+}
+
+template <class SH>
+cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
+    using LY = BwdLayout<SH>;
+    const size_t smem = LY::smem_bytes(prm.M);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    auto kern = prm.stream ? sig_bwd_kernel<SH, true> : sig_bwd_kernel<SH, false>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<(unsigned)prm.B, LY::NT, smem, st>>>(prm);
+    return cudaGetLastError();
+}
+
+}  // namespace sigb200

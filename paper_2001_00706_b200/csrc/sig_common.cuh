@@ -1,0 +1,223 @@
+// sig_common.cuh -- compile-time shapes and small device helpers shared by the sm_100a kernels.
+//
+// Truncated tensor layout: levels k = 1..N are
+// stored back to back; inside level k the word (j_1..j_k) (0-based letters) is at offset
+// sum_m j_m C^(k-m).  The scalar level 0 is implicit.
+//
+// Work decomposition: a thread owns one word prefix p = (p_0..p_{P-1}) of length
+// P.  It holds in registers every coefficient whose word starts with p, i.e. the contiguous block
+// of C^(k-P) floats at level k for every k >= max(P,1), plus one replicated copy of the prefix
+// coefficients A_i[p_0..p_{i-1}] for i < P.  The fused multiply-exponentiate (eq-fusedterm,
+// P:L164-167) for level k needs A_i only along the thread's own prefix below level P, so a thread
+// can advance its block with no communication at all.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+namespace sigb200 {
+
+__host__ __device__ __forceinline__ constexpr int64_t ipow(int64_t C, int k) {
+    int64_t r = 1;
+    for (int i = 0; i < k; ++i) r *= C;
+    return r;
+}
+
+template <int C_, int N_, int P_>
+struct Shape {
+    static constexpr int C = C_;
+    static constexpr int N = N_;
+    static constexpr int P = P_;
+    static constexpr int K0 = P_ > 1 ? P_ : 1;           // lowest owned level
+    static constexpr int CP = (int)ipow(C_, P_);         // threads per unit (one per prefix)
+    // number of owned coefficients at level k (k >= K0)
+    __host__ __device__ static constexpr int own(int k) { return (int)ipow(C_, k - P_); }
+    // register offset of level k inside the owned array
+    __host__ __device__ static constexpr int own_off(int k) {
+        int s = 0;
+        for (int j = K0; j < k; ++j) s += own(j);
+        return s;
+    }
+    static constexpr int OWN = own_off(N_ + 1);           // owned levels K0..N
+    static constexpr int OWN_BELOW_TOP = own_off(N_);     // owned levels K0..N-1
+    // flat offset of level k (1-based) in the S-wide layout
+    __host__ __device__ static constexpr int64_t lvl_off(int k) {
+        int64_t s = 0;
+        for (int j = 1; j < k; ++j) s += ipow(C_, j);
+        return s;
+    }
+    static constexpr int64_t S = lvl_off(N_ + 1);
+    static constexpr int NLOW = P_ > 1 ? P_ - 1 : 0;     // replicated prefix levels 1..P-1
+    // scratch for the Horner intermediates B_i, i = P+1..N-1 (C^(i-P) floats each)
+    __host__ __device__ static constexpr int tmp_off(int i) {
+        int s = 0;
+        for (int j = P_ + 1; j < i; ++j) s += own(j);
+        return s;
+    }
+    static constexpr int TMP = tmp_off(N_) > 0 ? tmp_off(N_) : 1;
+    static constexpr int LOWA = NLOW + 1;                 // low[1..P-1] (index 0 unused)
+    static constexpr int PD = P_ > 0 ? P_ : 1;            // digits array size
+    static constexpr int PL1 = P_ + 1;                    // arrays indexed 0..P
+    static constexpr int OWNA = OWN_BELOW_TOP > 0 ? OWN_BELOW_TOP : 1;
+};
+
+__host__ __device__ constexpr int ilog2(int v) {
+    int r = 0;
+    while ((1 << (r + 1)) <= v) ++r;
+    return r;
+}
+
+// compile-time loop: f(std::integral_constant<int, I>) for I in [B, E)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+template <class SH>
+__device__ __forceinline__ void prefix_digits(int prefix, int (&p)[SH::PD]) {
+    int r = prefix;
+#pragma unroll
+    for (int j = SH::P - 1; j >= 0; --j) {
+        p[j] = r % SH::C;
+        r /= SH::C;
+    }
+}
+
+// Store src[OFF .. OFF+n) (a register array: indices must stay compile-time constants so it is
+// never demoted to local memory) to dst, vectorised by the runtime alignment of dst.
+template <int n, int OFF, bool STREAMING, int SZ>
+__device__ __forceinline__ void store_run(float* dst, const float (&src)[SZ]) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+    if constexpr (n % 4 == 0) {
+        if ((a & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 4) {
+                float4 v = make_float4(src[OFF + i], src[OFF + i + 1], src[OFF + i + 2], src[OFF + i + 3]);
+                if (STREAMING) __stcs(reinterpret_cast<float4*>(dst + i), v);
+                else *reinterpret_cast<float4*>(dst + i) = v;
+            }
+            return;
+        }
+    }
+    if constexpr (n % 2 == 0) {
+        if ((a & 7) == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 2) {
+                float2 v = make_float2(src[OFF + i], src[OFF + i + 1]);
+                if (STREAMING) __stcs(reinterpret_cast<float2*>(dst + i), v);
+                else *reinterpret_cast<float2*>(dst + i) = v;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+        if (STREAMING) __stcs(dst + i, src[OFF + i]);
+        else dst[i] = src[OFF + i];
+    }
+}
+
+// Load n floats from src into dst[OFF .. OFF+n) (register array), vectorised by alignment.
+template <int n, int OFF, int SZ>
+__device__ __forceinline__ void load_run(float (&dst)[SZ], const float* src) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    if constexpr (n % 4 == 0) {
+        if ((a & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 4) {
+                float4 v = __ldg(reinterpret_cast<const float4*>(src + i));
+                dst[OFF + i] = v.x; dst[OFF + i + 1] = v.y; dst[OFF + i + 2] = v.z; dst[OFF + i + 3] = v.w;
+            }
+            return;
+        }
+    }
+    if constexpr (n % 2 == 0) {
+        if ((a & 7) == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 2) {
+                float2 v = __ldg(reinterpret_cast<const float2*>(src + i));
+                dst[OFF + i] = v.x; dst[OFF + i + 1] = v.y;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) dst[OFF + i] = __ldg(src + i);
+}
+
+// dst[OFF .. OFF+n) += src[0 .. n), vectorised by the alignment of src (no staging array).
+template <int n, int OFF, int SZ>
+__device__ __forceinline__ void add_run(float (&dst)[SZ], const float* src) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    if constexpr (n % 4 == 0) {
+        if ((a & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 4) {
+                float4 v = __ldg(reinterpret_cast<const float4*>(src + i));
+                dst[OFF + i] += v.x; dst[OFF + i + 1] += v.y; dst[OFF + i + 2] += v.z; dst[OFF + i + 3] += v.w;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) dst[OFF + i] += __ldg(src + i);
+}
+
+// reciprocals 1/s, s = 1..16 (exact float roundings of the rationals)
+__device__ __forceinline__ constexpr float inv_int(int s) {
+    return s == 1 ? 1.0f : 1.0f / (float)s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// mbarrier helpers (PTX ISA 8.x, sm_90+): shared-memory barriers used for the producer/consumer
+// ring between the high-level warps and the low-level warp of the backward kernel.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// 1-D bulk async copy global -> shared (TMA, cp.async.bulk), completion on an mbarrier.
+// Requires 16-byte aligned addresses and a byte count that is a multiple of 16.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+}  // namespace sigb200

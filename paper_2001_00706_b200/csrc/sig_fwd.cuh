@@ -1,0 +1,212 @@
+// sig_fwd.cuh -- K1: the fused multiply-exponentiate scan (forward signature), sm_100a.
+//
+// Method (Appendix A.1.2): Sig = exp(z_0) [x] exp(z_1) [x] ... is a
+// reduction with the fused operation A <- A [x] exp(z), whose level-k term is evaluated in
+// Horner form (eq-fusedterm):
+//     B_1 = z/k + A_1,   B_i = B_{i-1} (x) z/(k-i+1) + A_i  (i = 2..k),   A_k <- B_k,
+// for k = N down to 1, so that every A_i read while updating level k is still the old value.
+// The first exponential is the same update applied to the identity (A = 0).
+//
+// B200 design: FP32 FMA on the CUDA cores (no contraction dimension here, so
+// tensor cores do not apply), state register-resident with the prefix decomposition described in
+// sig_common.cuh -- no inter-thread communication inside the scan.  Increments are staged into
+// shared memory per tile; every thread reads the same z_t (broadcast LDS).  A "unit" is one time
+// chunk of one path ("splitting the computation up into chunks"); chunk results are
+// folded afterwards by the combine kernels (K3).
+#pragma once
+#include "sig_common.cuh"
+
+namespace sigb200 {
+
+struct FwdParams {
+    const float* path;       // [B, L, C]
+    const float* basepoint;  // [B, C] when bp_mode == 2
+    int bp_mode;             // 0 none, 1 zero, 2 given  (reading R4)
+    int stream;              // 1: write every prefix
+    int64_t B, L;
+    int64_t M;               // increments per path = L - 1 + (bp_mode != 0)
+    int64_t chunk_len;       // increments per unit
+    int64_t n_chunks;        // units per path (stream => 1)
+    int64_t n_units;         // B * n_chunks
+    int tile;                // increments staged per tile
+    float* out;              // stream: [B, M, S]; else unit u -> out + u * S
+};
+
+// Depth-first walk of the thread's word tree for the level-K Horner chain (eq-fusedterm):
+// node (I, W) is the word p.W at level I (W indexes the C^(I-P) words below the prefix), BI is
+// B_I[p.W].  Children: B_{I+1}[p.W.c] = B_I[p.W] * z_c / (K-I) + A_{I+1}[p.W.c]; at I+1 = K the
+// child is A_K itself, updated in place.  Walking depth-first keeps one chain value per level live
+// (a breadth-first sweep would hold whole blocks of B_i in registers).
+template <class SH, int K, int I, int W, bool NEG, int SZ>
+__device__ __forceinline__ void horner_visit(float BI, float (&own)[SZ], const float (&z)[SH::C]) {
+    constexpr int C = SH::C;
+    constexpr float sg = NEG ? -1.0f : 1.0f;  // NEG: multiply by -z (the reversibility step)
+    const float bs = (K - I == 1) ? sg * BI : BI * (sg * inv_int(K - I));
+    static_for<0, C>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        constexpr int child = W * C + c;
+        if constexpr (I + 1 == K) {
+            own[SH::own_off(K) + child] = fmaf(bs, z[c], own[SH::own_off(K) + child]);
+        } else {
+            const float Bc = fmaf(bs, z[c], own[SH::own_off(I + 1) + child]);
+            horner_visit<SH, K, I + 1, child, NEG>(Bc, own, z);
+        }
+    });
+}
+
+// b = B^(k)_P[p] along the thread's own prefix (B_0 = 1): the scalar part of the chain.
+template <class SH, int K, bool NEG, int SZ>
+__device__ __forceinline__ float prefix_chain(const float (&own)[SZ], const float (&low)[SH::LOWA],
+                                              const float (&zp)[SH::PD]) {
+    constexpr int P = SH::P;
+    constexpr float sg = NEG ? -1.0f : 1.0f;
+    float b = 1.0f;
+    static_for<1, P + 1>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        float Ai;
+        if constexpr (i < P) Ai = low[i];
+        else Ai = own[SH::own_off(P)];
+        if constexpr (i == 1) b = fmaf(zp[0], sg * inv_int(K), Ai);
+        else b = fmaf(b * (sg * inv_int(K - i + 1)), zp[i - 1], Ai);
+    });
+    return b;
+}
+
+// A <- A [x] exp(z) on owned levels KTOP..K0 (top-down) and then on the replicated prefix levels
+// P-1..1.  own: owned coefficients (levels K0..KTOP or more); low[i] (i = 1..P-1): A_i[p_0..p_{i-1}];
+// z[c]: the increment; zp[j] = z[p_j].  With z negated this is the reversibility step
+// (eq-reverse) used by the backward.
+template <class SH, int KTOP, bool NEG, int SZ>
+__device__ __forceinline__ void fused_mulexp(float (&own)[SZ], float (&low)[SH::LOWA], const float (&z)[SH::C],
+                                             const float (&zp)[SH::PD]) {
+    constexpr int P = SH::P;
+    constexpr float sg = NEG ? -1.0f : 1.0f;
+    static_for<0, (KTOP >= SH::K0 ? KTOP - SH::K0 + 1 : 0)>([&](auto kkc) {
+        constexpr int k = KTOP - decltype(kkc)::value;
+        const float b = prefix_chain<SH, k, NEG>(own, low, zp);
+        if constexpr (k == P) own[SH::own_off(P)] = b;
+        else horner_visit<SH, k, P, 0, NEG>(b, own, z);
+    });
+    static_for<0, (P > 1 ? P - 1 : 0)>([&](auto kkc) {
+        constexpr int k = P - 1 - decltype(kkc)::value;
+        float b = 1.0f;
+        static_for<1, k + 1>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if constexpr (i == 1) b = fmaf(zp[0], sg * inv_int(k), low[i]);
+            else b = fmaf(b * (sg * inv_int(k - i + 1)), zp[i - 1], low[i]);
+        });
+        low[k] = b;
+    });
+}
+
+// Write the thread's coefficients of the current state to a row of S floats.
+template <class SH, bool STREAMING>
+__device__ __forceinline__ void store_state(float* row, int prefix, const float (&own)[SH::OWN],
+                                            const float (&low)[SH::LOWA]) {
+    static_for<SH::K0, SH::N + 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        store_run<SH::own(k), SH::own_off(k), STREAMING>(row + SH::lvl_off(k) + (int64_t)prefix * SH::own(k), own);
+    });
+    // replicated prefix level i is written by the thread whose trailing digits are zero
+    static_for<1, SH::P>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        constexpr int tail = (int)ipow(SH::C, SH::P - i);
+        if (prefix % tail == 0) row[SH::lvl_off(i) + prefix / tail] = low[i];
+    });
+}
+
+template <class SH>
+__global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
+    constexpr int C = SH::C;
+    extern __shared__ float zs[];  // [units in CTA][tile][C]
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t gt = g0 + threadIdx.x;
+    const int64_t unit = gt / SH::CP;
+    const int prefix = (int)(gt % SH::CP);
+    const int64_t unit0 = g0 / SH::CP;
+    const int64_t unit1 = (g0 + blockDim.x - 1) / SH::CP;
+    const int nu = (int)(unit1 - unit0 + 1);
+    const int ul = (int)(unit - unit0);
+    const bool valid = unit < prm.n_units;
+    const int64_t b = valid ? unit / prm.n_chunks : 0;
+    const int64_t j = valid ? unit % prm.n_chunks : 0;
+    const int64_t s0 = j * prm.chunk_len;
+    const int64_t my_len = valid ? (prm.chunk_len < prm.M - s0 ? prm.chunk_len : prm.M - s0) : 0;
+    const int T = prm.tile;
+    const int has_bp = prm.bp_mode != 0;
+
+    int p[SH::PD];
+    prefix_digits<SH>(prefix, p);
+
+    float own[SH::OWN];
+    float low[SH::LOWA];
+#pragma unroll
+    for (int i = 0; i < SH::OWN; ++i) own[i] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < SH::LOWA; ++i) low[i] = 0.0f;
+
+    for (int64_t t0 = 0; t0 < prm.chunk_len; t0 += T) {
+        __syncthreads();
+        // ---- stage increments z = X[s+1] - X[s] of this tile for the CTA's units
+        const int nel = nu * T * C;
+        for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+            const int c = e % C;
+            const int t = (e / C) % T;
+            const int uu = e / (C * T);
+            const int64_t un = unit0 + uu;
+            float zv = 0.0f;
+            if (un < prm.n_units) {
+                const int64_t bb = un / prm.n_chunks, jj = un % prm.n_chunks;
+                const int64_t s = jj * prm.chunk_len + t0 + t;
+                if (t0 + t < prm.chunk_len && s < prm.M) {
+                    const float* xr = prm.path + bb * prm.L * C;
+                    // augmented point r: r == 0 is the basepoint when one is given
+                    const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
+                    const float x1 = xr[r1 * C + c];
+                    float x0;
+                    if (r0 >= 0) x0 = xr[r0 * C + c];
+                    else x0 = (prm.bp_mode == 2) ? prm.basepoint[bb * C + c] : 0.0f;
+                    zv = x1 - x0;
+                }
+            }
+            zs[e] = zv;
+        }
+        __syncthreads();
+        const int tl = (int)((int64_t)T < prm.chunk_len - t0 ? (int64_t)T : prm.chunk_len - t0);
+        const float* zrow = zs + (size_t)ul * T * C;
+        for (int t = 0; t < tl; ++t) {
+            if (t0 + t >= my_len) break;
+            float z[C];
+            float zp[SH::PD];
+#pragma unroll
+            for (int c = 0; c < C; ++c) z[c] = zrow[t * C + c];
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zp[q] = (SH::P > 0) ? zrow[t * C + p[q]] : 0.0f;
+            fused_mulexp<SH, SH::N, false>(own, low, z, zp);
+            if (prm.stream) {
+                float* row = prm.out + ((size_t)b * prm.M + (s0 + t0 + t)) * SH::S;
+                store_state<SH, true>(row, prefix, own, low);
+            }
+        }
+    }
+    if (valid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
+}
+
+template <class SH>
+cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
+    FwdParams prm = prm_in;
+    const int64_t threads = prm.n_units * (int64_t)SH::CP;
+    int bd = 512;
+    // small problems: spread over more SMs (latency-bound, e.g. BASELINE config c1)
+    while (bd > 32 && (threads + bd - 1) / bd < 148) bd /= 2;
+    const int64_t grid = (threads + bd - 1) / bd;
+    const int nu = (int)((bd - 1) / SH::CP + 2);  // max units touched by one CTA
+    int tile = (int)(prm.chunk_len < 256 ? prm.chunk_len : 256);
+    while (tile > 8 && (size_t)nu * tile * SH::C * 4 > 48 * 1024) tile /= 2;
+    prm.tile = tile;
+    const size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
+    sig_fwd_kernel<SH><<<(unsigned)grid, bd, smem, st>>>(prm);
+    return cudaGetLastError();
+}
+
+}  // namespace sigb200

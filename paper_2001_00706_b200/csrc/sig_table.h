@@ -1,0 +1,43 @@
+// sig_table.h -- dispatch table entries produced by gen_instances.py (one per supported (C, N)).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace sigb200 {
+
+struct FwdParams;
+struct BwdParams;
+
+using FwdLaunch = cudaError_t (*)(const FwdParams&, cudaStream_t);
+using BwdLaunch = cudaError_t (*)(const BwdParams&, cudaStream_t);
+
+struct KernelSet {
+    int C, N;
+    int pf0, pf1, pb;   // prefix lengths of the two forward variants and of the backward (-1: none)
+    FwdLaunch fwd0, fwd1;
+    BwdLaunch bwd;
+};
+
+const KernelSet* kernels_c1(int N);
+const KernelSet* kernels_c2(int N);
+const KernelSet* kernels_c3(int N);
+const KernelSet* kernels_c4(int N);
+const KernelSet* kernels_c5(int N);
+const KernelSet* kernels_c6(int N);
+const KernelSet* kernels_c7(int N);
+const KernelSet* kernels_c8(int N);
+
+inline const KernelSet* find_kernels(int C, int N) {
+    switch (C) {
+        case 1: return kernels_c1(N);
+        case 2: return kernels_c2(N);
+        case 3: return kernels_c3(N);
+        case 4: return kernels_c4(N);
+        case 5: return kernels_c5(N);
+        case 6: return kernels_c6(N);
+        case 7: return kernels_c7(N);
+        case 8: return kernels_c8(N);
+        default: return nullptr;
+    }
+}
+
+}  // namespace sigb200

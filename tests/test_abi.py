@@ -1,0 +1,68 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every symbol declared in
+include/sig.h, and its host-side queries and argument validation behave as documented."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sig.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2001_00706_b200 as sb
+    if not os.path.exists(sb.LIB_PATH):
+        from paper_2001_00706_b200 import build
+        build.build()
+    return sb.lib()
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sig_[a-z_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert len(names) >= 17, names
+    for n in names:
+        assert hasattr(L, n), f"{n} declared in include/sig.h but not exported"
+
+
+def test_sizes(L):
+    import paper_2001_00706_b200 as sb
+    assert sb.sig_signature_channels(8, 5) == 37448
+    assert sb.sig_signature_channels(4, 7) == 21844
+    assert sb.sig_signature_channels(0, 3) == -1
+    assert sb.sig_signature_channels(2, 70) == -1  # overflow
+    assert sb.sig_logsignature_channels(4, 7, "words") == 3304
+    assert sb.sig_logsignature_channels(8, 5, "brackets") == 7764
+    assert sb.sig_logsignature_channels(3, 6, "expand") == 1092
+    assert sb.sig_is_supported(8, 5, True) and sb.sig_is_supported(4, 7, True)
+    assert sb.sig_is_supported(3, 6) and sb.sig_is_supported(6, 4) and sb.sig_is_supported(4, 4)
+    assert not sb.sig_is_supported(9, 3)
+
+
+def test_validation_before_launch(L):
+    """Invalid arguments return an error code before anything touches the device."""
+    s = L.sig_signature(None, 2, 5, 3, 4, 0, 0, None, None, None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_INVALID_ARG"
+    s = L.sig_signature(ctypes.c_void_p(16), 2, 1, 3, 4, 0, 0, None, ctypes.c_void_p(16), None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_SHAPE"      # one point, no basepoint
+    assert b"2 points" in L.sig_last_error()
+    s = L.sig_signature(ctypes.c_void_p(16), 2, 5, 3, 0, 0, 0, None, ctypes.c_void_p(16), None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_INVALID_ARG"  # depth 0
+    s = L.sig_signature(ctypes.c_void_p(16), 2, 5, 9, 3, 0, 0, None, ctypes.c_void_p(16), None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_UNSUPPORTED"  # C = 9 not instantiated
+    s = L.sig_signature(ctypes.c_void_p(16), 2, 5, 3, 4, 0, 2, None, ctypes.c_void_p(16), None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_INVALID_ARG"  # GIVEN basepoint but NULL
+
+
+def test_workspace_query(L):
+    # a single long path is split into time chunks -> needs workspace; a big batch does not
+    assert L.sig_signature_workspace_size(1, 2 ** 22, 3, 6, 0, 0) > 0
+    assert L.sig_signature_workspace_size(1024, 128, 8, 5, 0, 0) == 0
+    assert L.sig_signature_workspace_size(256, 1024, 6, 4, 1, 0) == 0  # stream mode is never chunked

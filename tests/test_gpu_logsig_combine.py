@@ -1,0 +1,128 @@
+"""GPU parity for the logsignature (K4/K5) and the combine kernels (K3) against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import lyndon
+from synth import brownian_paths, normal
+from tests.parity import BWD_TOL, FWD_TOL, block_rel_err, level_rel_err, path_rel_err
+
+pytestmark = pytest.mark.gpu
+sb = pytest.importorskip("paper_2001_00706_b200")
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _blocks(C, N, mode):
+    if mode == "expand":
+        out, off = [], 0
+        for k in range(1, N + 1):
+            out.append((off, off + C ** k))
+            off += C ** k
+        return out
+    lv = [len(w) for w in lyndon.lyndon_words(C, N)]
+    return [(lv.index(k), len(lv) - lv[::-1].index(k)) for k in range(1, N + 1) if k in lv]
+
+
+LOG_CASES = [(4, 7, 4, 64), (3, 4, 5, 30), (2, 5, 6, 20), (8, 3, 3, 40), (4, 4, 8, 128)]
+
+
+@pytest.mark.parametrize("mode", ["words", "brackets", "expand"])
+@pytest.mark.parametrize("C,N,B,L", LOG_CASES)
+def test_logsignature_forward(mode, C, N, B, L):
+    x = brownian_paths(B, L, C, seed=C + N)
+    got = sb.sig_logsignature(_cuda(x), N, mode).cpu().numpy()
+    ref = oracle.logsignature(x, N, mode=mode, threads=8)
+    assert got.shape == ref.shape
+    err = block_rel_err(got, ref, _blocks(C, N, mode))
+    print(f"PARITY logsig fwd {mode} C={C} N={N} B={B} L={L}: {err:.3e}")
+    assert err < FWD_TOL
+
+
+@pytest.mark.parametrize("mode", ["words", "brackets", "expand"])
+@pytest.mark.parametrize("C,N,B,L", [(4, 7, 3, 48), (3, 4, 4, 20), (2, 5, 3, 15), (8, 3, 2, 30)])
+def test_logsignature_backward(mode, C, N, B, L):
+    x = brownian_paths(B, L, C, seed=3 * C + N)
+    w = sb.sig_logsignature_channels(C, N, mode)
+    g = normal((B, w), seed=104)
+    xt = _cuda(x).requires_grad_(True)
+    out = sb.logsignature(xt, N, mode)
+    out.backward(_cuda(g))
+    ref, _ = oracle.logsignature_vjp(g, x, N, mode=mode, threads=8)
+    err = path_rel_err(xt.grad.cpu().numpy(), ref)
+    print(f"PARITY logsig bwd {mode} C={C} N={N} B={B} L={L}: {err:.3e}")
+    assert err < BWD_TOL
+
+
+def test_logsignature_one_channel_exact_zeros():
+    """C = 1: the logsignature is (x_L - x_1, 0, ..., 0) exactly (one channel commutes); the zero
+    levels are checked absolutely against the scale of the signature level they come from."""
+    x = brownian_paths(2, 9, 1, seed=3)
+    for mode in ("words", "brackets", "expand"):
+        got = sb.sig_logsignature(_cuda(x), 3, mode).cpu().numpy()
+        d = (x[:, -1, 0] - x[:, 0, 0]).astype(np.float64)
+        np.testing.assert_allclose(got[:, 0], d, rtol=1e-5, atol=1e-6)
+        if got.shape[1] > 1:
+            assert np.max(np.abs(got[:, 1:])) < 1e-5 * max(1.0, float(np.max(np.abs(d))) ** 3)
+
+
+def test_logsignature_stream_and_single_segment():
+    C, N, B, L = 3, 4, 2, 12
+    x = brownian_paths(B, L, C, seed=9)
+    got = sb.sig_logsignature(_cuda(x), N, "words", stream=True).cpu().numpy()
+    ref = oracle.logsignature(x, N, mode="words", stream=True)
+    assert block_rel_err(got, ref, _blocks(C, N, "words")) < FWD_TOL
+    seg = np.array([[[0.0, 0.0], [0.7, -1.3]]], dtype=np.float32)
+    out = sb.sig_logsignature(_cuda(seg), 3, "brackets").cpu().numpy()[0]
+    np.testing.assert_allclose(out[:2], [0.7, -1.3], rtol=1e-6)
+    assert np.max(np.abs(out[2:])) < 1e-6
+
+
+def test_c4_full_size_sampled():
+    """BASELINE config c4 (B=512, L=256, C=4, N=7, words) full batch fwd+bwd, every 32nd path checked."""
+    C, N, B, L = 4, 7, 512, 256
+    x = brownian_paths(B, L, C, seed=4)
+    g = normal((B, 3304), seed=104)
+    xt = _cuda(x).requires_grad_(True)
+    out = sb.logsignature(xt, N, "words")
+    out.backward(_cuda(g))
+    idx = np.arange(0, B, 32)
+    ref = oracle.logsignature(x[idx], N, mode="words", threads=16)
+    ef = block_rel_err(out.detach().cpu().numpy()[idx], ref, _blocks(C, N, "words"))
+    rg, _ = oracle.logsignature_vjp(g[idx], x[idx], N, mode="words", threads=16)
+    eb = path_rel_err(xt.grad.cpu().numpy()[idx], rg)
+    print(f"PARITY c4 full-size sampled: fwd {ef:.3e} bwd {eb:.3e}")
+    assert ef < FWD_TOL and eb < BWD_TOL
+
+
+@pytest.mark.parametrize("C,N,B", [(3, 4, 5), (8, 5, 2), (2, 7, 3), (4, 1, 4)])
+def test_combine_and_backward(C, N, B):
+    S = sum(C ** k for k in range(1, N + 1))
+    xa = brownian_paths(B, 9, C, seed=1)
+    xb = brownian_paths(B, 7, C, seed=2)
+    a = oracle.signature(xa, N).astype(np.float32)
+    b = oracle.signature(xb, N).astype(np.float32)
+    got = sb.sig_signature_combine(_cuda(a), _cuda(b), C, N).cpu().numpy()
+    ref = oracle.combine(a, b, C, N)
+    assert level_rel_err(got, ref, C, N) < FWD_TOL
+    g = normal((B, S), seed=3)
+    ga, gb = sb.sig_signature_combine_backward(_cuda(g), _cuda(a), _cuda(b), C, N)
+    ra = np.stack([oracle.mul_vjp(g[i], a[i], b[i], C, N)[0] for i in range(B)])
+    rb = np.stack([oracle.mul_vjp(g[i], a[i], b[i], C, N)[1] for i in range(B)])
+    assert path_rel_err(ga.cpu().numpy(), ra) < BWD_TOL
+    assert path_rel_err(gb.cpu().numpy(), rb) < BWD_TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 40, 129])
+def test_multi_combine_chen(n):
+    """Folding the signatures of consecutive pieces equals the signature of the whole (Chen)."""
+    C, N, B = 3, 4, 3
+    pieces = n
+    L = 4 * pieces + 1
+    x = brownian_paths(B, L, C, seed=n)
+    sigs = np.stack([oracle.signature(x[:, 4 * j:4 * j + 5], N) for j in range(pieces)]).astype(np.float32)
+    got = sb.multi_signature_combine(_cuda(sigs), C, N).cpu().numpy()
+    assert level_rel_err(got, oracle.signature(x, N), C, N) < FWD_TOL

@@ -1,0 +1,174 @@
+"""GPU parity: the sm_100a signature forward/backward (through the C ABI) against the float64 oracle
+on the same seeded float32 inputs.  Bars: 1e-4 (forward, per path and level) and 5e-4 (backward,
+per path), BASELINE.json north_star; metric in tests/parity.py."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import brownian_paths, normal, uniform_paths
+from tests.parity import BWD_TOL, FWD_TOL, level_rel_err, path_rel_err
+
+pytestmark = pytest.mark.gpu
+
+sb = pytest.importorskip("paper_2001_00706_b200")
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+FWD_CASES = [
+    # (C, N, B, L, kind)
+    (4, 4, 32, 128, "brownian"),     # BASELINE config c1, full size
+    (4, 4, 32, 128, "uniform"),
+    (8, 5, 16, 128, "brownian"),     # c2 shape, subset of the batch
+    (8, 5, 5, 37, "uniform"),
+    (6, 4, 7, 100, "brownian"),      # c3 shape
+    (4, 7, 6, 64, "brownian"),       # c4 shape
+    (3, 6, 3, 333, "brownian"),      # c5 shape, short
+    (2, 3, 9, 17, "uniform"),
+    (1, 5, 4, 11, "monotone"),
+    (5, 3, 13, 29, "uniform"),
+    (7, 4, 3, 21, "brownian"),
+    (8, 2, 70, 9, "uniform"),
+    (3, 1, 5, 6, "brownian"),
+    (2, 8, 3, 40, "brownian"),
+    (4, 2, 1, 2, "uniform"),         # a single increment: exp(z)
+]
+
+
+def _paths(kind, B, L, C, seed):
+    if kind == "monotone":  # no cancellation between increments (used for C = 1, R9)
+        return np.cumsum(np.abs(brownian_paths(B, L, C, seed)), axis=1, dtype=np.float64).astype(np.float32)
+    return brownian_paths(B, L, C, seed) if kind == "brownian" else uniform_paths(B, L, C, seed + 1000)
+
+
+@pytest.mark.parametrize("C,N,B,L,kind", FWD_CASES)
+def test_forward_parity(C, N, B, L, kind):
+    x = _paths(kind, B, L, C, seed=C * 100 + N)
+    got = sb.sig_signature(_cuda(x), N).cpu().numpy()
+    ref = oracle.signature(x, N, threads=8)
+    assert got.shape == ref.shape
+    err = level_rel_err(got, ref, C, N)
+    print(f"PARITY fwd C={C} N={N} B={B} L={L} {kind}: {err:.3e}")
+    assert err < FWD_TOL, err
+
+
+@pytest.mark.parametrize("C,N,B,L", [(6, 4, 5, 60), (4, 4, 3, 33), (8, 3, 4, 20), (3, 6, 2, 41)])
+def test_forward_stream_parity(C, N, B, L):
+    x = brownian_paths(B, L, C, seed=7 + C)
+    got = sb.sig_signature(_cuda(x), N, stream=True).cpu().numpy()
+    ref = oracle.signature(x, N, stream=True, threads=8)
+    assert got.shape == (B, L - 1, sum(C ** k for k in range(1, N + 1)))
+    assert level_rel_err(got, ref, C, N) < FWD_TOL
+
+
+@pytest.mark.parametrize("bp", ["zero", "given"])
+def test_forward_basepoint(bp):
+    C, N, B, L = 4, 4, 6, 25
+    x = brownian_paths(B, L, C, seed=3)
+    bpv = normal((B, C), seed=4, scale=0.3)
+    arg = True if bp == "zero" else _cuda(bpv)
+    oarg = True if bp == "zero" else bpv
+    got = sb.sig_signature(_cuda(x), N, basepoint=arg).cpu().numpy()
+    ref = oracle.signature(x, N, basepoint=oarg)
+    assert level_rel_err(got, ref, C, N) < FWD_TOL
+    # a single point with a basepoint
+    got1 = sb.sig_signature(_cuda(x[:, :1]), N, basepoint=arg).cpu().numpy()
+    ref1 = oracle.signature(x[:, :1], N, basepoint=oarg)
+    assert level_rel_err(got1, ref1, C, N) < FWD_TOL
+
+
+def test_long_path_time_chunked():
+    """One long path: the library splits it into time chunks and folds them with [x] in order."""
+    C, N, L = 3, 6, 40000
+    x = brownian_paths(1, L, C, seed=5)
+    got = sb.sig_signature(_cuda(x), N).cpu().numpy()
+    ref = oracle.signature(x, N)
+    assert level_rel_err(got, ref, C, N) < FWD_TOL
+    x2 = brownian_paths(3, 9001, 2, seed=6)  # ragged chunking, several paths
+    got2 = sb.sig_signature(_cuda(x2), 5).cpu().numpy()
+    assert level_rel_err(got2, oracle.signature(x2, 5, threads=3), 2, 5) < FWD_TOL
+
+
+def test_empty_batch_and_determinism():
+    x = brownian_paths(0, 10, 3, seed=1)
+    assert sb.sig_signature(_cuda(x), 3).shape == (0, 39)
+    y = _cuda(brownian_paths(64, 128, 8, seed=2))
+    a = sb.sig_signature(y, 5)
+    b = sb.sig_signature(y, 5)
+    assert torch.equal(a, b)
+
+
+BWD_CASES = [
+    (4, 4, 16, 32, False),
+    (8, 5, 8, 128, False),   # c2 shape
+    (4, 7, 4, 64, False),    # c4 shape
+    (3, 6, 3, 50, False),
+    (2, 3, 5, 12, False),
+    (1, 3, 2, 6, False),
+    (5, 4, 3, 20, False),
+    (6, 4, 2, 30, True),
+    (4, 4, 3, 16, True),
+    (8, 3, 4, 25, False),
+    (3, 1, 4, 5, False),
+]
+
+
+@pytest.mark.parametrize("C,N,B,L,stream", BWD_CASES)
+def test_backward_parity(C, N, B, L, stream):
+    x = brownian_paths(B, L, C, seed=11 * C + N)
+    S = sum(C ** k for k in range(1, N + 1))
+    g = normal((B, L - 1, S) if stream else (B, S), seed=100 + C)
+    xt = _cuda(x)
+    out = sb.sig_signature(xt, N, stream=stream)
+    gp, _ = sb.sig_signature_backward(_cuda(g), xt, out, N, stream=stream)
+    ref, _ = oracle.signature_vjp(g, x, N, stream=stream, threads=8)
+    err = path_rel_err(gp.cpu().numpy(), ref)
+    print(f"PARITY bwd C={C} N={N} B={B} L={L} stream={stream}: {err:.3e}")
+    assert err < BWD_TOL, err
+
+
+def test_backward_basepoint_given_and_autograd():
+    C, N, B, L = 4, 5, 4, 20
+    x = brownian_paths(B, L, C, seed=21)
+    bp = normal((B, C), seed=22, scale=0.2)
+    g = normal((B, sum(C ** k for k in range(1, N + 1))), seed=23)
+    xt = _cuda(x).requires_grad_(True)
+    bpt = _cuda(bp).requires_grad_(True)
+    out = sb.signature(xt, N, basepoint=bpt)
+    out.backward(_cuda(g))
+    rx, rb = oracle.signature_vjp(g, x, N, basepoint=bp)
+    assert path_rel_err(xt.grad.cpu().numpy(), rx) < BWD_TOL
+    assert path_rel_err(bpt.grad.cpu().numpy(), rb) < BWD_TOL
+
+
+def test_paper_code_example():
+    """signatory.signature(torch.rand(1, 10, 2), 4).sum().backward()."""
+    torch.manual_seed(0)
+    path = torch.rand(1, 10, 2, device="cuda", requires_grad=True)
+    sig = sb.signature(path, 4)
+    sig.sum().backward()
+    x = path.detach().cpu().numpy()
+    assert level_rel_err(sig.detach().cpu().numpy(), oracle.signature(x, 4), 2, 4) < FWD_TOL
+    ref, _ = oracle.signature_vjp(np.ones((1, 30)), x, 4)
+    assert path_rel_err(path.grad.cpu().numpy(), ref) < BWD_TOL
+
+
+def test_c2_full_size_sampled():
+    """BASELINE config c2 at full size (B=1024, L=128, C=8, N=5) in the launch configuration bench.py
+    times: forward + backward of the whole batch, every 64th path checked against the oracle."""
+    C, N, B, L = 8, 5, 1024, 128
+    x = brownian_paths(B, L, C, seed=2)
+    g = normal((B, 37448), seed=102)
+    xt = _cuda(x)
+    out = sb.sig_signature(xt, N)
+    gp, _ = sb.sig_signature_backward(_cuda(g), xt, out, N)
+    idx = np.arange(0, B, 64)
+    ref = oracle.signature(x[idx], N, threads=16)
+    ef = level_rel_err(out.cpu().numpy()[idx], ref, C, N)
+    rg, _ = oracle.signature_vjp(g[idx], x[idx], N, threads=16)
+    eb = path_rel_err(gp.cpu().numpy()[idx], rg)
+    print(f"PARITY c2 full-size sampled: fwd {ef:.3e} bwd {eb:.3e}")
+    assert ef < FWD_TOL and eb < BWD_TOL
