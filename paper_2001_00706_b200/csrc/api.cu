@@ -281,8 +281,8 @@ LogsigTables device_view(const sig_logsig_plan_s* pl) {
     return tb;
 }
 
-sig_status_t check_logsig_smem(const TensorDims& d, int64_t w) {
-    if (logsig_fwd_smem(d, (int)w) > 227 * 1024 || logsig_bwd_smem(d) > 227 * 1024)
+sig_status_t check_logsig_smem(const TensorDims& d, int64_t w, bool brackets) {
+    if (logsig_fwd_smem(d, (int)w, brackets) > 227 * 1024 || logsig_bwd_smem(d) > 227 * 1024)
         return fail(SIG_ERR_UNSUPPORTED, "logsignature of C=%d depth=%d exceeds one CTA's shared memory", d.C, d.N);
     return SIG_OK;
 }
@@ -441,7 +441,7 @@ sig_status_t sig_logsig_plan_create(int64_t C, int32_t depth, sig_logsig_mode_t 
     pl->mode = mode;
     pl->S = d.S;
     pl->w = (mode == SIG_LOGSIG_EXPAND) ? d.S : witt_dimension(C, depth);
-    sig_status_t st = check_logsig_smem(d, pl->w);
+    sig_status_t st = check_logsig_smem(d, pl->w, mode == SIG_LOGSIG_BRACKETS);
     if (st != SIG_OK) return st;
     cudaGetDevice(&pl->dt.device);
     if (mode != SIG_LOGSIG_EXPAND) {
@@ -520,7 +520,7 @@ sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t
     p.rows = rows;
     p.sig = sig;
     p.out = out;
-    const size_t smem = logsig_fwd_smem(p.d, (int)plan->w);
+    const size_t smem = logsig_fwd_smem(p.d, (int)plan->w, p.mode == 1);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(logsig_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_status(e, "logsig smem attribute");

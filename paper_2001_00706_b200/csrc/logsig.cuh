@@ -8,9 +8,12 @@
 // BRACKETS = (psi o phi)^{-1} psi(log) as a sparse mat-vec with the exact integer
 // inverse built on the host; EXPAND = log itself.
 //
-// One CTA per signature row; x and the H_n live in shared memory.  The work is ~N*S FMAs per row
-// (about 2-5% of the scan at the BASELINE shapes), so this is a latency-bound epilogue, not a
-// roofline kernel.  The backward (K5) walks the Horner recursion in reverse and produces the
+// One CTA per signature row; x (float, as stored) and the H_n (double) live in shared memory.
+// The series cancels heavily at deep levels (at C=4, N=7 the float evaluation loses ~1e-4
+// relative at level 7 while the log is well conditioned in its input: ~1e-6), so the
+// arithmetic of K4/K5 is float64 with float32 inputs and outputs.  The work is
+// ~N*S FMAs per row (about 2-5% of the scan at the BASELINE shapes): a latency-bound epilogue,
+// not a roofline kernel.  The backward (K5) walks the Horner recursion in reverse and produces the
 // dense gradient w.r.t. the signature that seeds the reversible signature backward (K2).
 #pragma once
 #include "combine.cuh"
@@ -47,11 +50,11 @@ __device__ __forceinline__ int64_t hoff(const TensorDims& d, int m) {  // levels
 }
 
 // (x H)_k[w] = sum_{i=1}^{k} x_i[w / C^(k-i)] H_{k-i}[w mod C^(k-i)]   (H given on levels 0..k-1)
-__device__ __forceinline__ float xh_coef(const TensorDims& d, const float* xs, const float* H, int k, int64_t w) {
-    float acc = 0.0f;
+__device__ __forceinline__ double xh_coef(const TensorDims& d, const float* xs, const double* H, int k, int64_t w) {
+    double acc = 0.0;
     for (int i = 1; i <= k; ++i) {
         const int64_t q = d.pw[k - i];
-        acc = fmaf(xs[d.off[i] + w / q], H[hoff(d, k - i) + w % q], acc);
+        acc = fma((double)xs[d.off[i] + w / q], H[hoff(d, k - i) + w % q], acc);
     }
     return acc;
 }
@@ -61,33 +64,31 @@ __global__ void logsig_fwd_kernel(const LogsigParams p) {
     const int N = d.N;
     const int64_t S = d.S;
     const int64_t row = blockIdx.x;
-    extern __shared__ float ls[];
+    extern __shared__ __align__(16) double lsd[];
     const int64_t HS = hoff(d, N);  // levels 0..N-1
-    float* xs = ls;
-    float* Ha = xs + S;
-    float* Hb = Ha + HS;
-    float* psi = Hb + HS;  // [w] (brackets)
+    double* Ha = lsd;
+    double* Hb = Ha + HS;
+    float* xs = reinterpret_cast<float*>(Hb + HS);  // [S]
+    float* psi = xs + S;                            // [w] (brackets only)
     const float* src = p.sig + row * S;
     for (int64_t f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
-    if (threadIdx.x == 0) Ha[0] = 1.0f / (float)N;
+    if (threadIdx.x == 0) Ha[0] = 1.0 / (double)N;
     __syncthreads();
-    float* Hc = Ha;
-    float* Hn = Hb;
+    double* Hc = Ha;
+    double* Hn = Hb;
     for (int n = N - 1; n >= 1; --n) {
         const int top = N - n;  // H_n on levels 0..top
-        const float cn = 1.0f / (float)n;
         for (int64_t e = threadIdx.x; e < hoff(d, top + 1); e += blockDim.x) {
             if (e == 0) {
-                Hn[0] = cn;
+                Hn[0] = 1.0 / (double)n;
                 continue;
             }
             int m = 1;
             while (e >= hoff(d, m + 1)) ++m;
-            const int64_t v = e - hoff(d, m);
-            Hn[e] = -xh_coef(d, xs, Hc, m, v);
+            Hn[e] = -xh_coef(d, xs, Hc, m, e - hoff(d, m));
         }
         __syncthreads();
-        float* t = Hc;
+        double* t = Hc;
         Hc = Hn;
         Hn = t;
     }
@@ -96,20 +97,21 @@ __global__ void logsig_fwd_kernel(const LogsigParams p) {
         float* o = p.out + row * S;
         for (int64_t f = threadIdx.x; f < S; f += blockDim.x) {
             const int k = level_of(d, f);
-            o[f] = xh_coef(d, xs, Hc, k, f - d.off[k]);
+            o[f] = (float)xh_coef(d, xs, Hc, k, f - d.off[k]);
         }
         return;
     }
     float* o = p.out + row * p.tb.w;
-    float* dst = (p.mode == 2) ? o : psi;
     for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
         const int64_t f = p.tb.lyn_idx[j];
         const int k = level_of(d, f);
-        dst[j] = xh_coef(d, xs, Hc, k, f - d.off[k]);
+        const double v = xh_coef(d, xs, Hc, k, f - d.off[k]);
+        if (p.mode == 2) o[j] = (float)v;
+        else psi[j] = (float)v;
     }
     if (p.mode == 1) {
         __syncthreads();
-        // exact integer coefficients with heavy cancellation: accumulate in fp64 (K4)
+        // exact integer coefficients of (psi o phi)^{-1}
         for (int r = threadIdx.x; r < p.tb.w; r += blockDim.x) {
             double acc = 0.0;
             for (int e = p.tb.minv_rowptr[r]; e < p.tb.minv_rowptr[r + 1]; ++e)
@@ -130,28 +132,27 @@ __global__ void logsig_bwd_kernel(const LogsigParams p) {
     const int N = d.N;
     const int64_t S = d.S;
     const int64_t row = blockIdx.x;
-    extern __shared__ float ls[];
+    extern __shared__ __align__(16) double lsd[];
     const int64_t HS = hoff(d, N);
-    float* xs = ls;
-    float* Hall = xs + S;  // H_n at hb(n), levels 0..N-n
-    auto hb = [&](int n) -> int64_t {
+    auto hb = [&](int n) -> int64_t {  // offset of H_n (levels 0..N-n) in Hall
         int64_t s = 0;
         for (int q = N; q > n; --q) s += hoff(d, N - q + 1);
         return s;
     };
-    float* gHa = Hall + hb(0);
-    float* gHb = gHa + HS;
+    double* Hall = lsd;
+    double* gH = Hall + hb(0);                      // [HS] gradient of the current H_n (in place)
+    float* xs = reinterpret_cast<float*>(gH + HS);  // [S]
     const float* src = p.sig + row * S;
     for (int64_t f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
-    if (threadIdx.x == 0) Hall[hb(N)] = 1.0f / (float)N;
+    if (threadIdx.x == 0) Hall[hb(N)] = 1.0 / (double)N;
     __syncthreads();
     for (int n = N - 1; n >= 1; --n) {
         const int top = N - n;
-        float* Hn = Hall + hb(n);
-        const float* Hc = Hall + hb(n + 1);
+        double* Hn = Hall + hb(n);
+        const double* Hc = Hall + hb(n + 1);
         for (int64_t e = threadIdx.x; e < hoff(d, top + 1); e += blockDim.x) {
             if (e == 0) {
-                Hn[0] = 1.0f / (float)n;
+                Hn[0] = 1.0 / (double)n;
                 continue;
             }
             int m = 1;
@@ -160,7 +161,7 @@ __global__ void logsig_bwd_kernel(const LogsigParams p) {
         }
         __syncthreads();
     }
-    // dense dL/dlog
+    // dense dL/dlog (float32 in the workspace for words/brackets)
     const float* g;
     if (p.mode == 0) {
         g = p.gout + row * S;
@@ -170,16 +171,15 @@ __global__ void logsig_bwd_kernel(const LogsigParams p) {
         __syncthreads();
         const float* go = p.gout + row * p.tb.w;
         for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
-            float v;
+            double v;
             if (p.mode == 2) {
                 v = go[j];
             } else {
-                double a = 0.0;
+                v = 0.0;
                 for (int e = p.tb.minvT_rowptr[j]; e < p.tb.minvT_rowptr[j + 1]; ++e)
-                    a = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], a);
-                v = (float)a;
+                    v = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], v);
             }
-            gw[p.tb.lyn_idx[j]] = v;
+            gw[p.tb.lyn_idx[j]] = (float)v;
         }
         __syncthreads();
         g = gw;
@@ -187,79 +187,74 @@ __global__ void logsig_bwd_kernel(const LogsigParams p) {
     float* gx = p.gsig + row * S;
     // step A: log = x H_1 (H_1 on levels 0..N-1)
     {
-        const float* H1 = Hall + hb(1);
+        const double* H1 = Hall + hb(1);
         for (int64_t f = threadIdx.x; f < S; f += blockDim.x) {
             const int i = level_of(d, f);
             const int64_t u = f - d.off[i];
-            float acc = 0.0f;
+            double acc = 0.0;
             for (int m = 0; m <= N - i; ++m) {
                 const int64_t nv = d.pw[m];
                 const float* gk = g + d.off[i + m] + u * nv;
-                const float* hm = H1 + hoff(d, m);
-                for (int64_t v = 0; v < nv; ++v) acc = fmaf(gk[v], hm[v], acc);
+                const double* hm = H1 + hoff(d, m);
+                for (int64_t v = 0; v < nv; ++v) acc = fma((double)gk[v], hm[v], acc);
             }
-            gx[f] = acc;
+            gx[f] = (float)acc;
         }
         for (int64_t e = threadIdx.x; e < HS; e += blockDim.x) {
             if (e == 0) continue;
             int m = 1;
             while (e >= hoff(d, m + 1)) ++m;
             const int64_t v = e - hoff(d, m);
-            float acc = 0.0f;
+            double acc = 0.0;
             for (int i = 1; i <= N - m; ++i) {
                 const int64_t nu = d.pw[i];
                 const float* gk = g + d.off[i + m] + v;
                 const float* xi = xs + d.off[i];
-                for (int64_t u = 0; u < nu; ++u) acc = fmaf(xi[u], gk[u * d.pw[m]], acc);
+                for (int64_t u = 0; u < nu; ++u) acc = fma((double)xi[u], (double)gk[u * d.pw[m]], acc);
             }
-            gHa[e] = acc;
+            gH[e] = acc;
         }
         __syncthreads();
     }
-    float* gc = gHa;
-    float* gn = gHb;
     for (int n = 1; n <= N - 1; ++n) {
-        const int top = N - n;  // gH_n on levels 1..top
-        const float* Hnext = Hall + hb(n + 1);  // levels 0..top-1
+        const int top = N - n;  // gH = dL/dH_n on levels 1..top
+        const double* Hnext = Hall + hb(n + 1);  // levels 0..top-1
         for (int64_t f = threadIdx.x; f < d.off[top + 1]; f += blockDim.x) {
             const int i = level_of(d, f);
             const int64_t u = f - d.off[i];
-            float acc = 0.0f;
+            double acc = 0.0;
             for (int m = 0; m <= top - i; ++m) {
                 const int64_t nv = d.pw[m];
-                const float* gk = gc + hoff(d, i + m) + u * nv;
-                const float* hm = Hnext + hoff(d, m);
-                for (int64_t v = 0; v < nv; ++v) acc = fmaf(gk[v], hm[v], acc);
+                const double* gk = gH + hoff(d, i + m) + u * nv;
+                const double* hm = Hnext + hoff(d, m);
+                for (int64_t v = 0; v < nv; ++v) acc = fma(gk[v], hm[v], acc);
             }
-            gx[f] -= acc;
-        }
-        if (n <= N - 2) {
-            for (int64_t e = threadIdx.x; e < hoff(d, top); e += blockDim.x) {
-                if (e == 0) continue;
-                int m = 1;
-                while (e >= hoff(d, m + 1)) ++m;
-                const int64_t v = e - hoff(d, m);
-                float acc = 0.0f;
-                for (int i = 1; i <= top - m; ++i) {
-                    const int64_t nu = d.pw[i];
-                    const float* gk = gc + hoff(d, i + m) + v;
-                    const float* xi = xs + d.off[i];
-                    for (int64_t u = 0; u < nu; ++u) acc = fmaf(xi[u], gk[u * d.pw[m]], acc);
-                }
-                gn[e] = -acc;
-            }
+            gx[f] = (float)((double)gx[f] - acc);
         }
         __syncthreads();
-        float* t = gc;
-        gc = gn;
-        gn = t;
+        // dL/dH_{n+1} in place, level by level upward: level m reads only levels > m
+        if (n <= N - 2) {
+            for (int m = 1; m <= top - 1; ++m) {
+                for (int64_t v = threadIdx.x; v < d.pw[m]; v += blockDim.x) {
+                    double acc = 0.0;
+                    for (int i = 1; i <= top - m; ++i) {
+                        const int64_t nu = d.pw[i];
+                        const double* gk = gH + hoff(d, i + m) + v;
+                        const float* xi = xs + d.off[i];
+                        for (int64_t u = 0; u < nu; ++u) acc = fma((double)xi[u], gk[u * d.pw[m]], acc);
+                    }
+                    gH[hoff(d, m) + v] = -acc;
+                }
+                __syncthreads();
+            }
+        }
     }
 }
 
-inline size_t logsig_fwd_smem(const TensorDims& d, int w) {
+inline size_t logsig_fwd_smem(const TensorDims& d, int w, bool brackets) {
     int64_t HS = 0;
     for (int j = 0; j < d.N; ++j) HS += d.pw[j];
-    return (size_t)(d.S + 2 * HS + w) * sizeof(float);
+    return (size_t)(2 * HS) * sizeof(double) + (size_t)(d.S + (brackets ? w : 0)) * sizeof(float);
 }
 
 inline size_t logsig_bwd_smem(const TensorDims& d) {
@@ -268,7 +263,7 @@ inline size_t logsig_bwd_smem(const TensorDims& d) {
     int64_t hall = 0;
     for (int n = 1; n <= d.N; ++n)
         for (int j = 0; j <= d.N - n; ++j) hall += d.pw[j];
-    return (size_t)(d.S + hall + 2 * HS) * sizeof(float);
+    return (size_t)(hall + HS) * sizeof(double) + (size_t)d.S * sizeof(float);
 }
 
 }  // namespace sigb200
