@@ -71,9 +71,9 @@ def dist_signature_timechunk(x_local: torch.Tensor, depth: int, group=None,
         s_local = torch.zeros((B, S), dtype=x_local.dtype, device=x_local.device)
     if world == 1:
         return s_local
-    gathered = torch.empty((world,) + tuple(s_local.shape), dtype=s_local.dtype, device=s_local.device)
-    dist.all_gather_into_tensor(gathered, s_local, group=group)  # rank order == time order
-    return fold(gathered, C, depth)
+    flat = torch.empty(world * s_local.numel(), dtype=s_local.dtype, device=s_local.device)
+    dist.all_gather_into_tensor(flat, s_local.reshape(-1), group=group)  # rank order == time order
+    return fold(flat.view((world,) + tuple(s_local.shape)), C, depth)
 
 
 def dist_signature_batch(x_local: torch.Tensor, depth: int, local_sig: Optional[Callable] = None) -> torch.Tensor:

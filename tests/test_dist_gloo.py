@@ -33,20 +33,26 @@ def _oracle_fold(sigs, C, depth):
     return torch.from_numpy(oracle.multi_combine(sigs.numpy(), C, depth))
 
 
+def _work(rank, world, L, C, N):
+    x = brownian_paths(2, L, C, seed=42)
+    a, b = sdist.time_chunk_bounds(L, world, rank)
+    xl = torch.from_numpy(x[:, a:b].astype(np.float64))
+    sig = sdist.dist_signature_timechunk(xl, N, local_sig=_oracle_sig, fold=_oracle_fold)
+    # batch sharding: each rank its own slice, no collective
+    lo, hi = sdist.batch_bounds(5, world, rank)
+    xb = brownian_paths(5, 9, C, seed=7)
+    sb = sdist.dist_signature_batch(torch.from_numpy(xb[lo:hi].astype(np.float64)), N, local_sig=_oracle_sig)
+    return rank, sig.numpy(), lo, hi, sb.numpy()
+
+
 def _worker(rank, world, port, L, C, N, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        x = brownian_paths(2, L, C, seed=42)
-        a, b = sdist.time_chunk_bounds(L, world, rank)
-        xl = torch.from_numpy(x[:, a:b].astype(np.float64))
-        sig = sdist.dist_signature_timechunk(xl, N, local_sig=_oracle_sig, fold=_oracle_fold)
-        # batch sharding: each rank its own slice, no collective
-        lo, hi = sdist.batch_bounds(5, world, rank)
-        xb = brownian_paths(5, 9, C, seed=7)
-        sb = sdist.dist_signature_batch(torch.from_numpy(xb[lo:hi].astype(np.float64)), N, local_sig=_oracle_sig)
-        q.put((rank, sig.numpy(), lo, hi, sb.numpy()))
+        q.put(_work(rank, world, L, C, N))
+    except Exception as e:  # surface worker failures instead of hanging the parent
+        q.put((rank, repr(e), None, None, None))
     finally:
         dist.destroy_process_group()
 
@@ -60,7 +66,9 @@ def test_timechunk_and_batch_world2(L):
     procs = [ctx.Process(target=_worker, args=(r, world, port, L, C, N, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    res = [q.get(timeout=180) for _ in range(world)]
+    for r in res:
+        assert not isinstance(r[1], str), r[1]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
