@@ -29,7 +29,8 @@ __all__ = [
     "BP_NONE", "BP_ZERO", "BP_GIVEN", "MODES",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsig.so")
+# SIGB200_LIB may point at an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("SIGB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsig.so")
 BP_NONE, BP_ZERO, BP_GIVEN = 0, 1, 2
 MODES = {"expand": 0, "brackets": 1, "words": 2}
 

@@ -17,8 +17,11 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build_obj")
-LIB = os.path.join(HERE, "libsig.so")
+# SIGB200_BUILD_TAG builds a variant (extra -D flags from SIGB200_EXTRA_FLAGS) into libsig_<tag>.so
+_TAG = os.environ.get("SIGB200_BUILD_TAG", "")
+OBJ = os.path.join(HERE, "build_obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(HERE, f"libsig_{_TAG}.so" if _TAG else "libsig.so")
+_EXTRA = os.environ.get("SIGB200_EXTRA_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--extended-lambda", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -40,7 +43,7 @@ def _compile(src: str, force: bool, hdr_t: float) -> tuple[str, str]:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
         return obj, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *_EXTRA, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC, "-x", "c++", *FLAGS[:4], "-Xcompiler", "-fPIC", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -72,23 +72,44 @@ struct BwdLayout {
 template <class SH, int K, int I, int W, int SA>
 __device__ __forceinline__ float vjp_visit(float BI, float (&G)[SH::OWN], const float (&A)[SA], const float (&z)[SH::C],
                                            float (&gz)[SH::C]) {
+    // channel pairs with the packed FFMA2 (see horner_visit): gz += bs * x and acc += x * z
     constexpr int C = SH::C;
     constexpr float sc = inv_int(K - I);
     const float bs = BI * sc;
-    float acc = 0.0f;
-    static_for<0, C>([&](auto cc) {
-        constexpr int c = decltype(cc)::value;
-        constexpr int child = W * C + c;
+    const float2 bs2 = make_float2(bs, bs);
+    float2 acc2 = make_float2(0.0f, 0.0f);
+    static_for<0, C / 2>([&](auto cc) {
+        constexpr int c = 2 * decltype(cc)::value;
+        constexpr int ch = W * C + c;
+        const float2 z2 = make_float2(z[c], z[c + 1]);
+        float2 x;
+        if constexpr (I + 1 == K) {
+            x = make_float2(G[SH::own_off(K) + ch], G[SH::own_off(K) + ch + 1]);
+        } else {
+            constexpr int o = SH::own_off(I + 1) + ch;
+            const float2 Bc = __ffma2_rn(bs2, z2, make_float2(A[o], A[o + 1]));
+            x.x = vjp_visit<SH, K, I + 1, ch>(Bc.x, G, A, z, gz);
+            x.y = vjp_visit<SH, K, I + 1, ch + 1>(Bc.y, G, A, z, gz);
+        }
+        const float2 g2 = __ffma2_rn(bs2, x, make_float2(gz[c], gz[c + 1]));
+        gz[c] = g2.x;
+        gz[c + 1] = g2.y;
+        acc2 = __ffma2_rn(x, z2, acc2);
+    });
+    float acc = acc2.x + acc2.y;
+    if constexpr (C % 2 == 1) {
+        constexpr int c = C - 1;
+        constexpr int ch = W * C + c;
         float x;
         if constexpr (I + 1 == K) {
-            x = G[SH::own_off(K) + child];
+            x = G[SH::own_off(K) + ch];
         } else {
-            const float Bc = fmaf(bs, z[c], A[SH::own_off(I + 1) + child]);
-            x = vjp_visit<SH, K, I + 1, child>(Bc, G, A, z, gz);
+            const float Bc = fmaf(bs, z[c], A[SH::own_off(I + 1) + ch]);
+            x = vjp_visit<SH, K, I + 1, ch>(Bc, G, A, z, gz);
         }
         gz[c] = fmaf(bs, x, gz[c]);
         acc = fmaf(x, z[c], acc);
-    });
+    }
     const float beta = acc * sc;
     if constexpr (I >= SH::K0) G[SH::own_off(I) + W] += beta;
     return beta;

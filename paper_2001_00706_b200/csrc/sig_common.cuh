@@ -17,6 +17,16 @@
 
 namespace sigb200 {
 
+#ifndef SIG_ZSWZ
+#define SIG_ZSWZ 0
+#endif
+// Increments are staged in shared memory with adjacent channels swapped (c <-> c^1 when C is
+// even), so that a vector LDS.128 of a staged row puts z_c in a register whose parity differs from
+// that of the state coefficients ending in letter c (which vector LDG/STG keep in natural order).
+// The FFMA z_c * b + A[..c] then reads its two non-reused operands from different register banks
+// (two same-parity register sources halve the FFMA issue rate; K1).
+__host__ __device__ constexpr int zswz(int C, int c) { return (SIG_ZSWZ && C % 2 == 0) ? (c ^ 1) : c; }
+
 __host__ __device__ __forceinline__ constexpr int64_t ipow(int64_t C, int k) {
     int64_t r = 1;
     for (int i = 0; i < k; ++i) r *= C;

@@ -39,19 +39,40 @@ struct FwdParams {
 // (a breadth-first sweep would hold whole blocks of B_i in registers).
 template <class SH, int K, int I, int W, bool NEG, int SZ>
 __device__ __forceinline__ void horner_visit(float BI, float (&own)[SZ], const float (&z)[SH::C]) {
+    // Channels are processed in pairs with the packed FFMA2 (fma.rn.f32x2): the same FLOP rate as
+    // FFMA in half the issue slots (measured, scripts/fma_peak.cu), which matters because the
+    // scan is issue-bound.  z and the owned blocks sit in natural order, so (c, c+1) pairs are
+    // aligned register pairs straight from the vector loads.
     constexpr int C = SH::C;
     constexpr float sg = NEG ? -1.0f : 1.0f;  // NEG: multiply by -z (the reversibility step)
     const float bs = (K - I == 1) ? sg * BI : BI * (sg * inv_int(K - I));
-    static_for<0, C>([&](auto cc) {
-        constexpr int c = decltype(cc)::value;
-        constexpr int child = W * C + c;
+    const float2 bs2 = make_float2(bs, bs);
+    static_for<0, C / 2>([&](auto cc) {
+        constexpr int c = 2 * decltype(cc)::value;
+        constexpr int ch = W * C + c;
+        const float2 z2 = make_float2(z[c], z[c + 1]);
         if constexpr (I + 1 == K) {
-            own[SH::own_off(K) + child] = fmaf(bs, z[c], own[SH::own_off(K) + child]);
+            constexpr int o = SH::own_off(K) + ch;
+            const float2 r = __ffma2_rn(bs2, z2, make_float2(own[o], own[o + 1]));
+            own[o] = r.x;
+            own[o + 1] = r.y;
         } else {
-            const float Bc = fmaf(bs, z[c], own[SH::own_off(I + 1) + child]);
-            horner_visit<SH, K, I + 1, child, NEG>(Bc, own, z);
+            constexpr int o = SH::own_off(I + 1) + ch;
+            const float2 Bc = __ffma2_rn(bs2, z2, make_float2(own[o], own[o + 1]));
+            horner_visit<SH, K, I + 1, ch, NEG>(Bc.x, own, z);
+            horner_visit<SH, K, I + 1, ch + 1, NEG>(Bc.y, own, z);
         }
     });
+    if constexpr (C % 2 == 1) {
+        constexpr int c = C - 1;
+        constexpr int ch = W * C + c;
+        if constexpr (I + 1 == K) {
+            own[SH::own_off(K) + ch] = fmaf(bs, z[c], own[SH::own_off(K) + ch]);
+        } else {
+            const float Bc = fmaf(bs, z[c], own[SH::own_off(I + 1) + ch]);
+            horner_visit<SH, K, I + 1, ch, NEG>(Bc, own, z);
+        }
+    }
 }
 
 // b = B^(k)_P[p] along the thread's own prefix (B_0 = 1): the scalar part of the chain.
@@ -169,19 +190,26 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
                     zv = x1 - x0;
                 }
             }
-            zs[e] = zv;
+            zs[e - c + zswz(C, c)] = zv;  // pair-swapped staging (see zswz)
         }
         __syncthreads();
         const int tl = (int)((int64_t)T < prm.chunk_len - t0 ? (int64_t)T : prm.chunk_len - t0);
+        const int tn = (int)((int64_t)tl < my_len - t0 ? (int64_t)tl : (my_len - t0 > 0 ? my_len - t0 : 0));
+        // running pointers into the staged increments: z_t and the thread's prefix letters z_t[p_q]
         const float* zrow = zs + (size_t)ul * T * C;
-        for (int t = 0; t < tl; ++t) {
-            if (t0 + t >= my_len) break;
+        const float* zq[SH::PD];
+#pragma unroll
+        for (int q = 0; q < SH::PD; ++q) zq[q] = zrow + (SH::P > 0 ? zswz(C, p[q]) : 0);
+        for (int t = 0; t < tn; ++t) {
             float z[C];
             float zp[SH::PD];
 #pragma unroll
-            for (int c = 0; c < C; ++c) z[c] = zrow[t * C + c];
+            for (int c = 0; c < C; ++c) z[c] = zrow[zswz(C, c)];
 #pragma unroll
-            for (int q = 0; q < SH::PD; ++q) zp[q] = (SH::P > 0) ? zrow[t * C + p[q]] : 0.0f;
+            for (int q = 0; q < SH::PD; ++q) zp[q] = *zq[q];
+            zrow += C;
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zq[q] += C;
             fused_mulexp<SH, SH::N, false>(own, low, z, zp);
             if (prm.stream) {
                 float* row = prm.out + ((size_t)b * prm.M + (s0 + t0 + t)) * SH::S;
