@@ -120,13 +120,24 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 def cpu_baseline(cfg_name: str, seconds: float = 15.0) -> dict:
     """The float64 oracle (test infrastructure, as it stands) on the host cores: a bounded sample
-    of the same workload (the first paths of the same seeded batch), threads = all cores."""
+    of the same workload (the first paths of the same seeded batch; for the single long path of c5
+    a prefix of it, scaled to whole paths), threads = all cores."""
     import oracle
 
     cfg = CONFIGS[cfg_name]
     C, N, L = cfg["C"], cfg["N"], cfg["L"]
     cores = os.cpu_count() or 1
     ps, gs = SEEDS[cfg_name]
+    if cfg_name == "c5":
+        Ls = 2 ** 17 + 1
+        x = brownian_paths(1, L, C, ps)[:, :Ls]
+        t0 = time.perf_counter()
+        _oracle_step(oracle, cfg_name, x, gs, 1)
+        dt = time.perf_counter() - t0
+        frac = (Ls - 1) / (L - 1)
+        return {"value": frac / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"first {Ls} of {L} points of the c5 path (float64 C oracle, 1 thread: the scan is "
+                          f"sequential), {dt:.1f} s, scaled by {frac:.4f}"}
     # size the sample from a 1-path probe so the run stays within ~`seconds`
     x1 = brownian_paths(1, L, C, ps)
     t0 = time.perf_counter()
@@ -139,7 +150,7 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0) -> dict:
     _oracle_step(oracle, cfg_name, x, gs, cores)
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": UNIT, "cores": min(cores, n), "kind": "oracle",
-            "sample": f"{n} of {cfg['B']} paths of {cfg_name} (fwd+bwd, float64 C oracle, {min(cores, n)} threads), "
+            "sample": f"{n} of {cfg['B']} paths of {cfg_name} ({cfg['op']}, float64 C oracle, {min(cores, n)} threads), "
                       f"{dt:.1f} s"}
 
 
@@ -167,10 +178,19 @@ def run_reference(args, rank: int, world: int):
     import oracle
 
     cores = os.cpu_count() or 1
-    n = min(cfg["B"], max(cores, 16))
-    x = brownian_paths(cfg["B"], cfg["L"], cfg["C"], SEEDS[args.config][0])[:n]
+    if args.config == "c5":  # one long path: each step is a bounded prefix, scaled to whole paths
+        Ls = 2 ** 16 + 1
+        x = brownian_paths(1, cfg["L"], cfg["C"], SEEDS["c5"][0])[:, :Ls]
+        n = (Ls - 1) / (cfg["L"] - 1)
+        sample = f"first {Ls} points of the c5 path per step (scaled), float64 C oracle, 1 thread"
+        used = 1
+    else:
+        n = min(cfg["B"], max(cores, 16))
+        x = brownian_paths(cfg["B"], cfg["L"], cfg["C"], SEEDS[args.config][0])[:n]
+        sample = f"{n} of {cfg['B']} paths per step, float64 C oracle, {min(cores, n)} threads"
+        used = min(cores, n)
     for _ in range(args.warmup):
-        _oracle_step(oracle, args.config, x[:cores], SEEDS[args.config][1], cores)
+        _oracle_step(oracle, args.config, x[: max(1, min(cores, x.shape[0]))], SEEDS[args.config][1], cores)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -183,8 +203,7 @@ def run_reference(args, rank: int, world: int):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(args.config, world),
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(cores, n), "kind": "oracle",
-                         "sample": f"{n} of {cfg['B']} paths per step, float64 C oracle, {min(cores, n)} threads"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -195,12 +214,148 @@ def _config_dict(name, world):
     return {"workload": f"{name}: {cfg['op']} B={cfg['B']}/GPU L={cfg['L']} C={cfg['C']} N={cfg['N']}"
                         f"{' stream' if cfg['stream'] else ''}, Brownian",
             "B_per_gpu": cfg["B"], "L": cfg["L"], "C": cfg["C"], "depth": cfg["N"], "stream": cfg["stream"],
-            "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"time-chunk x{world} (NCCL all-gather + ordered fold)" if name == "c5" else
+                            f"batch-shard x{world}") if world > 1 else "single GPU",
             "l2": "per-step working set > 126 MB L2 (grad_out + signature 307 MB); no flush needed"
             if name == "c2" else "see DESIGN.md"}
 
 
 # ------------------------------------------------------------------------------------------------
+class Workload:
+    """One BASELINE config as a benchmark step.  step(ev) runs one step on the device (ev: list of
+    (label, start_event, end_event) for the live per-kernel split, or None); e2e_step() runs it from
+    pinned host buffers; units = paths processed per step on this rank."""
+
+    def __init__(self, name, rank, world, dev):
+        import torch
+
+        import paper_2001_00706_b200 as sb
+
+        self.sb, self.torch, self.dev, self.name = sb, torch, dev, name
+        cfg = CONFIGS[name]
+        self.cfg = cfg
+        self.B, self.L, self.C, self.N = cfg["B"], cfg["L"], cfg["C"], cfg["N"]
+        self.S = sb.sig_signature_channels(self.C, self.N)
+        ps, gs = SEEDS[name]
+        self.world, self.rank = world, rank
+        if name == "c5":
+            from paper_2001_00706_b200 import dist as sdist
+
+            full = brownian_paths(1, self.L, self.C, ps)  # the one long path, time-chunked over ranks
+            a, b = sdist.time_chunk_bounds(self.L, world, rank)
+            self.x_np = np.ascontiguousarray(full[:, a:b])
+            self.M = b - a - 1
+            self.units = 1.0 / world  # one path per step for the whole job
+        else:
+            self.x_np = brownian_paths(self.B, self.L, self.C, ps + 7919 * rank)
+            self.M = self.L - 1
+            self.units = self.B
+        self.x = torch.from_numpy(self.x_np).to(dev)
+        self.g = None
+        if cfg["op"] == "sig_fwd_bwd":
+            self.g_np = normal((self.B, self.S), gs + 7919 * rank)
+        elif cfg["op"] == "logsig_words_fwd_bwd":
+            self.g_np = normal((self.B, sb.sig_logsignature_channels(self.C, self.N, "words")), gs + 7919 * rank)
+        else:
+            self.g_np = None
+        if self.g_np is not None:
+            self.g = torch.from_numpy(self.g_np).to(dev)
+        self.stream = torch.cuda.current_stream(dev)
+
+    def _run(self, x, g, ev):
+        sb, N, torch = self.sb, self.N, self.torch
+        rec = (lambda lab: ev.append((lab, torch.cuda.Event(enable_timing=True)))) if ev is not None else None
+
+        def mark(lab):
+            if ev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(self.stream)
+                ev.append((lab, e))
+
+        op = self.cfg["op"]
+        mark("start")
+        if op == "sig_fwd_bwd":
+            out = sb.sig_signature(x, N)
+            mark("fwd")
+            res, _ = sb.sig_signature_backward(g, x, out, N)
+            mark("bwd")
+        elif op == "logsig_words_fwd_bwd":
+            out, sig = sb.sig_logsignature(x, N, "words", return_signature=True)
+            mark("fwd")
+            res, _ = sb.sig_logsignature_backward(g, x, sig, N, "words")
+            mark("bwd")
+        elif op == "sig_fwd_timechunk":
+            from paper_2001_00706_b200 import dist as sdist
+
+            res = sdist.dist_signature_timechunk(x, N) if self.world > 1 else sb.sig_signature(x, N)
+            mark("fwd")
+        else:
+            res = sb.sig_signature(x, N, stream=self.cfg["stream"])
+            mark("fwd")
+        del rec
+        return res
+
+    def step(self, ev=None):
+        return self._run(self.x, self.g, ev)
+
+    def prepare_e2e(self):
+        torch = self.torch
+        self.xh = torch.from_numpy(self.x_np).pin_memory()
+        self.gh = torch.from_numpy(self.g_np).pin_memory() if self.g_np is not None else None
+        self.xd = torch.empty_like(self.x)
+        self.gd = torch.empty_like(self.g) if self.g is not None else None
+        res = self.step()
+        self.resh = torch.empty(res.shape, dtype=res.dtype).pin_memory()
+        self.h2d = self.xh.numel() * 4 + (self.gh.numel() * 4 if self.gh is not None else 0)
+        self.d2h = self.resh.numel() * 4
+
+    def e2e_step(self):
+        self.xd.copy_(self.xh, non_blocking=True)
+        if self.gh is not None:
+            self.gd.copy_(self.gh, non_blocking=True)
+        res = self._run(self.xd, self.gd, None)
+        self.resh.copy_(res, non_blocking=True)
+
+    def roofline(self, seg_ms, ms_step):
+        """Dominant kernel's roofline from the live per-segment CUDA-event times."""
+        C, N, M, B = self.C, self.N, self.M, (1 if self.name == "c5" else self.B)
+        peak, peak_src = fp32_peak_tflops()
+        op = self.cfg["op"]
+        traffic = None
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(self.name, {})
+        except Exception:
+            traffic = {}
+        if op in ("sig_fwd_bwd", "logsig_words_fwd_bwd"):
+            f_fwd = alg_flops("fwd", B, M, C, N)
+            f_bwd = alg_flops("bwd", B, M, C, N)
+            ach = f_bwd / (seg_ms["bwd"] / 1000) / 1e12
+            kern = ("sig_bwd_kernel (reversible backward)" if op == "sig_fwd_bwd"
+                    else "sig_logsignature_backward call = logsig_bwd_kernel + sig_bwd_kernel (sig-bwd FLOPs only)")
+            return {"bound": "alu", "kernel": kern, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                    "frac": ach / peak, "traffic": traffic.get("sig_bwd_kernel"), "peak_source": peak_src,
+                    "kernel_ms": seg_ms["bwd"], "step_share": seg_ms["bwd"] / (seg_ms["fwd"] + seg_ms["bwd"]),
+                    "fwd": {"kernel_ms": seg_ms["fwd"], "achieved": f_fwd / (seg_ms["fwd"] / 1000) / 1e12,
+                            "frac": f_fwd / (seg_ms["fwd"] / 1000) / 1e12 / peak},
+                    "step_frac": (f_fwd + f_bwd) / (ms_step / 1000) / 1e12 / peak}
+        if op == "sig_fwd_stream":
+            hbm = 6543.7
+            try:
+                hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            except Exception:
+                pass
+            nbytes = B * M * self.S * 4 + B * self.L * C * 4  # written prefixes + read path
+            ach = nbytes / (seg_ms["fwd"] / 1000) / 1e9
+            return {"bound": "hbm", "kernel": "sig_fwd_kernel (stream=True)", "achieved": ach, "peak": hbm,
+                    "unit": "GB/s", "frac": ach / hbm, "traffic": traffic.get("sig_fwd_kernel"),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel_ms": seg_ms["fwd"]}
+        f = alg_flops("fwd", B, M, C, N)
+        ach = f / (seg_ms["fwd"] / 1000) / 1e12
+        return {"bound": "alu", "kernel": "sig_fwd_kernel (+ ordered chunk fold" + (", NCCL all-gather)" if self.world > 1 else ")"),
+                "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": traffic.get("sig_fwd_kernel"), "peak_source": peak_src, "kernel_ms": seg_ms["fwd"]}
+
+
 def run_ours(args, rank: int, world: int):
     import torch
     import torch.distributed as dist
@@ -209,119 +364,76 @@ def run_ours(args, rank: int, world: int):
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    cfg = CONFIGS[args.config]
-    assert cfg["op"] == "sig_fwd_bwd", "bench.py times the metric's configuration c2 (see scripts/ for others)"
-    B, L, C, N = cfg["B"], cfg["L"], cfg["C"], cfg["N"]
-    S = sb.sig_signature_channels(C, N)
-    M = L - 1
-    ps, gs = SEEDS[args.config]
-    x_np = brownian_paths(B, L, C, ps + 7919 * rank)
-    g_np = normal((B, S), gs + 7919 * rank)
-    x = torch.from_numpy(x_np).to(dev)
-    g = torch.from_numpy(g_np).to(dev)
-    stream = torch.cuda.current_stream(dev)
-
+    wl = Workload(args.config, rank, world, dev)
+    stream = wl.stream
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    def step(times=None):
-        if times is not None:
-            e0, e1, e2 = ev(), ev(), ev()
-            e0.record(stream)
-        out = sb.sig_signature(x, N)
-        if times is not None:
-            e1.record(stream)
-        gp, _ = sb.sig_signature_backward(g, x, out, N)
-        if times is not None:
-            e2.record(stream)
-            times.append((e0, e1, e2))
-        return gp
-
     for _ in range(args.warmup):
-        step()
+        wl.step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     launches0 = sb.lib().sig_launch_count()
-    kt = []
+    splits = []
     sampler = ClockSampler(dev.index)
     with sampler:
         t_start, t_end = ev(), ev()
         t_start.record(stream)
         for i in range(args.steps):
-            step(kt if i % 4 == 0 else None)
+            if i % 4 == 0:
+                rec = []
+                wl.step(rec)
+                splits.append(rec)
+            else:
+                wl.step()
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     launches = sb.lib().sig_launch_count() - launches0
-    ms_total = t_start.elapsed_time(t_end)
-    ms_t = torch.tensor([ms_total], device=dev)
+    ms_t = torch.tensor([t_start.elapsed_time(t_end)], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_step = float(ms_t.item()) / args.steps
-    value = world * B / (ms_step / 1000.0)
+    value = world * wl.units / (ms_step / 1000.0)
+    seg = {}
+    for rec in splits:
+        for (la, ea), (lb, eb) in zip(rec, rec[1:]):
+            seg.setdefault(lb, []).append(ea.elapsed_time(eb))
+    seg_ms = {k: float(np.mean(v)) for k, v in seg.items()}
+    roofline = wl.roofline(seg_ms, ms_step)
 
-    fwd_ms = float(np.mean([a.elapsed_time(b) for a, b, _ in kt]))
-    bwd_ms = float(np.mean([b.elapsed_time(c) for _, b, c in kt]))
-    peak, peak_src = fp32_peak_tflops()
-    bwd_flops = alg_flops("bwd", B, M, C, N)
-    achieved = bwd_flops / (bwd_ms / 1000) / 1e12
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof.get("c2", {}).get("sig_bwd_kernel")
-    except Exception:
-        pass
-    roofline = {"bound": "alu", "kernel": "sig_bwd_kernel<Shape<8,5,3>> (reversible backward)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": peak_src, "kernel_ms": bwd_ms, "step_share": bwd_ms / (fwd_ms + bwd_ms),
-                "fwd": {"kernel": "sig_fwd_kernel<Shape<8,5,3>>", "kernel_ms": fwd_ms,
-                        "achieved": alg_flops("fwd", B, M, C, N) / (fwd_ms / 1000) / 1e12,
-                        "frac": alg_flops("fwd", B, M, C, N) / (fwd_ms / 1000) / 1e12 / peak},
-                "step_frac": (alg_flops("fwd", B, M, C, N) + bwd_flops) / (ms_step / 1000) / 1e12 / peak}
-
-    # ---- e2e through the C ABI from pinned host buffers
-    xh = torch.from_numpy(x_np).pin_memory()
-    gh = torch.from_numpy(g_np).pin_memory()
-    gph = torch.empty((B, L, C), dtype=torch.float32).pin_memory()
-    xd = torch.empty_like(x)
-    gd = torch.empty_like(g)
-
-    def e2e_step():
-        xd.copy_(xh, non_blocking=True)
-        gd.copy_(gh, non_blocking=True)
-        out = sb.sig_signature(xd, N)
-        gp, _ = sb.sig_signature_backward(gd, xd, out, N)
-        gph.copy_(gp, non_blocking=True)
-
+    # ---- e2e through the C ABI from pinned host buffers (H2D inputs, D2H result, every step)
+    wl.prepare_e2e()
     n_e2e = max(3, min(args.steps, 50))
     for _ in range(3):
-        e2e_step()
+        wl.e2e_step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     a, b = ev(), ev()
     a.record(stream)
     for _ in range(n_e2e):
-        e2e_step()
+        wl.e2e_step()
     b.record(stream)
     torch.cuda.synchronize(dev)
     e_ms = torch.tensor([a.elapsed_time(b) / n_e2e], device=dev)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e2e = {"value": world * B / (float(e_ms.item()) / 1000), "unit": UNIT,
-           "h2d_bytes_per_step": int(x.numel() * 4 + g.numel() * 4), "d2h_bytes_per_step": int(B * L * C * 4),
-           "path": "C ABI (sig_signature + sig_signature_backward) with pinned host buffers"}
+    e2e = {"value": world * wl.units / (float(e_ms.item()) / 1000), "unit": UNIT,
+           "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),
+           "path": "C ABI calls from pinned host buffers (inputs H2D, result D2H inside the timed region)"}
 
     if rank != 0:
         return
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": _config_dict(args.config, world), "roofline": roofline,
-        "e2e": e2e, "clocks": sampler.summary(), "gpu_launches": int(launches),
+        "metric": METRIC if args.config == "c2" else f"{CONFIGS[args.config]['op']} paths/sec ({args.config})",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if args.config == "c5" else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config_dict(args.config, world),
+        "roofline": roofline, "e2e": e2e, "clocks": sampler.summary(), "gpu_launches": int(launches),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, seconds=args.cpu_seconds)

@@ -55,6 +55,7 @@ int64_t sig_channels_checked(int64_t C, int32_t depth) {
 
 // ---------------------------------------------------------------- forward launch plan
 constexpr int64_t kTargetThreads = 148LL * 1024;  // ~2 resident waves of 512-thread CTAs
+constexpr int64_t kOneWave = 148LL * 512;          // one resident wave
 constexpr int64_t kMinChunk = 64;                 // increments per time chunk, at least
 
 struct FwdPlan {
@@ -108,12 +109,14 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
     pl.launch = ks->fwd0;
     const int64_t cp0 = sigb200::ipow(C, ks->pf0);
     pl.n_chunks = 1;
-    if (!stream && B > 0 && B * cp0 < kTargetThreads && M >= 2 * kMinChunk) {
+    // split long paths into time chunks only when the batch cannot fill one wave of the GPU
+    // (the fold costs a launch and a pass over the chunk signatures)
+    if (!stream && B > 0 && B * cp0 < kOneWave && M >= 2 * kMinChunk) {
         int64_t want = (kTargetThreads + B * cp0 - 1) / (B * cp0);
         int64_t maxc = M / kMinChunk;
         pl.n_chunks = want < maxc ? want : maxc;
     }
-    if (pl.n_chunks == 1 && B * cp0 < kTargetThreads && ks->fwd1) {
+    if (pl.n_chunks == 1 && B * cp0 < kOneWave && ks->fwd1) {
         pl.P = ks->pf1;
         pl.launch = ks->fwd1;
     }
@@ -281,7 +284,7 @@ LogsigTables device_view(const sig_logsig_plan_s* pl) {
     return tb;
 }
 
-sig_status_t check_logsig_smem(const TensorDims& d, int64_t w, bool brackets) {
+sig_status_t check_logsig_smem(const LDims& d, int64_t w, bool brackets) {
     if (logsig_fwd_smem(d, (int)w, brackets) > 227 * 1024 || logsig_bwd_smem(d) > 227 * 1024)
         return fail(SIG_ERR_UNSUPPORTED, "logsignature of C=%d depth=%d exceeds one CTA's shared memory", d.C, d.N);
     return SIG_OK;
@@ -374,6 +377,7 @@ sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, in
                                    sig_cuda_stream_t s) {
     const int64_t S = sig_channels_checked(C, depth);
     if (S < 0 || depth > 15) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (S >= (1LL << 28)) return fail(SIG_ERR_UNSUPPORTED, "signature of %lld floats too large", (long long)S);
     if (!a || !b || !out) return fail(SIG_ERR_INVALID_ARG, "a, b and out must be non-null");
     if (B < 0) return fail(SIG_ERR_SHAPE, "B < 0");
     if (B == 0) return ok();
@@ -389,6 +393,7 @@ sig_status_t sig_signature_combine_backward(const float* grad_out, const float* 
                                             sig_cuda_stream_t s) {
     const int64_t S = sig_channels_checked(C, depth);
     if (S < 0 || depth > 15) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (S >= (1LL << 28)) return fail(SIG_ERR_UNSUPPORTED, "signature of %lld floats too large", (long long)S);
     if (!grad_out || !a || !b) return fail(SIG_ERR_INVALID_ARG, "grad_out, a and b must be non-null");
     if (B < 0) return fail(SIG_ERR_SHAPE, "B < 0");
     if (B == 0 || (!grad_a && !grad_b)) return ok();
@@ -414,6 +419,7 @@ sig_status_t sig_multi_signature_combine(const float* sigs, int64_t n, int64_t B
                                          float* out, void* ws, size_t ws_bytes, sig_cuda_stream_t s) {
     const int64_t S = sig_channels_checked(C, depth);
     if (S < 0 || depth > 15) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (S >= (1LL << 28)) return fail(SIG_ERR_UNSUPPORTED, "signature of %lld floats too large", (long long)S);
     if (!sigs || !out) return fail(SIG_ERR_INVALID_ARG, "sigs and out must be non-null");
     if (n < 1 || B < 0) return fail(SIG_ERR_SHAPE, "n=%lld must be >= 1", (long long)n);
     const size_t need = sig_multi_signature_combine_workspace_size(n, B, C, depth);
@@ -434,7 +440,7 @@ sig_status_t sig_logsig_plan_create(int64_t C, int32_t depth, sig_logsig_mode_t 
         return fail(SIG_ERR_INVALID_ARG, "bad logsignature mode %d", (int)mode);
     if (!find_kernels((int)C, depth))
         return fail(SIG_ERR_UNSUPPORTED, "no sm_100a kernel instantiated for C=%lld depth=%d", (long long)C, depth);
-    const TensorDims d = make_dims((int)C, depth);
+    const LDims d = make_ldims((int)C, depth);
     auto pl = std::make_unique<sig_logsig_plan_s>();
     pl->C = (int)C;
     pl->N = depth;
@@ -514,7 +520,7 @@ sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t
     st = run_signature(path, B, L, plan->C, plan->N, stream, bp, basepoint, sig, ws, pl.ws_bytes, (cudaStream_t)s);
     if (st != SIG_OK) return st;
     LogsigParams p{};
-    p.d = make_dims(plan->C, plan->N);
+    p.d = make_ldims(plan->C, plan->N);
     p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
     p.tb = device_view(plan);
     p.rows = rows;
@@ -525,7 +531,7 @@ sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t
         cudaError_t e = cudaFuncSetAttribute(logsig_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_status(e, "logsig smem attribute");
     }
-    logsig_fwd_kernel<<<(unsigned)rows, 256, smem, (cudaStream_t)s>>>(p);
+    logsig_fwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, (cudaStream_t)s>>>(p);
     count_launch();
     return cuda_status(cudaGetLastError(), "logsig launch");
 }
@@ -551,7 +557,7 @@ sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad
     float* glog = reinterpret_cast<float*>(wsb) + (size_t)rows * plan->S;
     float* gsig = glog + (size_t)rows * plan->S;
     LogsigParams p{};
-    p.d = make_dims(plan->C, plan->N);
+    p.d = make_ldims(plan->C, plan->N);
     p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
     p.tb = device_view(plan);
     p.rows = rows;
@@ -564,7 +570,7 @@ sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad
         cudaError_t e = cudaFuncSetAttribute(logsig_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
     }
-    logsig_bwd_kernel<<<(unsigned)rows, 256, smem, (cudaStream_t)s>>>(p);
+    logsig_bwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, (cudaStream_t)s>>>(p);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");

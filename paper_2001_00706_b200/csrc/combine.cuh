@@ -18,11 +18,12 @@
 
 namespace sigb200 {
 
+// 32-bit level tables (signatures here have S < 2^31 and C^N < 2^24)
 struct TensorDims {
-    int C, N;
-    int64_t S;
-    int64_t off[17];   // off[k] = flat offset of level k (1-based), off[N+1] = S
-    int64_t pw[17];    // pw[k] = C^k
+    int C, N, S;
+    int off[18];     // off[k] = flat offset of level k (1-based), off[N+1] = S
+    int pw[17];      // pw[k] = C^k
+    uint32_t magic;  // n / C == __umulhi(n, magic) exactly for n < 2^32 / C
 };
 
 inline TensorDims make_dims(int C, int N) {
@@ -34,21 +35,27 @@ inline TensorDims make_dims(int C, int N) {
     d.off[1] = 0;
     for (int k = 1; k <= N; ++k) d.off[k + 1] = d.off[k] + d.pw[k];
     d.S = d.off[N + 1];
+    d.magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)C - 1) / (uint64_t)C);
     return d;
 }
 
-__device__ __forceinline__ int level_of(const TensorDims& d, int64_t f) {
+__device__ __forceinline__ int level_of(const TensorDims& d, int f) {
     int k = 1;
     while (k < d.N && f >= d.off[k + 1]) ++k;
     return k;
 }
 
-// out = a [x] b for one flat coefficient f (level k, word w)
-__device__ __forceinline__ float mul_coef(const TensorDims& d, const float* a, const float* b, int k, int64_t w) {
+// out = a [x] b for one flat coefficient (level k, word w): split w = u.v for |u| = i, i = k-1..1,
+// peeling one letter at a time (no division other than by C, done with the magic multiplier)
+__device__ __forceinline__ float mul_coef(const TensorDims& d, const float* a, const float* b, int k, int w) {
     float acc = a[d.off[k] + w] + b[d.off[k] + w];
-    for (int i = 1; i < k; ++i) {
-        const int64_t q = d.pw[k - i];
-        acc = fmaf(a[d.off[i] + w / q], b[d.off[k - i] + w % q], acc);
+    int u = w, v = 0, q = 1;
+    for (int i = k - 1; i >= 1; --i) {
+        const int u2 = (d.C == 1) ? u : (int)__umulhi((uint32_t)u, d.magic);
+        v += (u - u2 * d.C) * q;
+        q *= d.C;
+        u = u2;
+        acc = fmaf(a[d.off[i] + u], b[d.off[k - i] + v], acc);
     }
     return acc;
 }
@@ -57,7 +64,7 @@ __device__ __forceinline__ float mul_coef(const TensorDims& d, const float* a, c
 // row r: out + r*so = (a + r*sa) [x] (b + r*sb)
 __global__ void combine_pair_kernel(const TensorDims d, const float* __restrict__ a, int64_t sa,
                                     const float* __restrict__ b, int64_t sb, float* __restrict__ out, int64_t so) {
-    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t r = blockIdx.y;
     if (f >= d.S) return;
     const int k = level_of(d, f);
@@ -69,21 +76,21 @@ __global__ void combine_pair_kernel(const TensorDims d, const float* __restrict_
 //   gb_j[v] = go_j[v] + sum_{k>j} sum_u go_k[u v] a_{k-j}[u]
 __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restrict__ go, const float* __restrict__ a,
                                         const float* __restrict__ b, float* __restrict__ ga, float* __restrict__ gb) {
-    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t r = blockIdx.y;
     if (f >= d.S) return;
     const int i = level_of(d, f);
-    const int64_t u = f - d.off[i];
+    const int u = f - d.off[i];
     const float* gor = go + r * d.S;
     const float* ar = a + r * d.S;
     const float* br = b + r * d.S;
     if (ga) {
         float acc = gor[f];
         for (int k = i + 1; k <= d.N; ++k) {
-            const int64_t nv = d.pw[k - i];
+            const int nv = d.pw[k - i];
             const float* gk = gor + d.off[k] + u * nv;
             const float* bk = br + d.off[k - i];
-            for (int64_t v = 0; v < nv; ++v) acc = fmaf(gk[v], bk[v], acc);
+            for (int v = 0; v < nv; ++v) acc = fmaf(gk[v], bk[v], acc);
         }
         ga[r * d.S + f] = acc;
     }
@@ -91,11 +98,11 @@ __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restr
         // f indexes level j = i, word v = u
         float acc = gor[f];
         for (int k = i + 1; k <= d.N; ++k) {
-            const int64_t nu = d.pw[k - i];
-            const int64_t stride = d.pw[i];
+            const int nu = d.pw[k - i];
+            const int stride = d.pw[i];
             const float* gk = gor + d.off[k] + u;
             const float* ak = ar + d.off[k - i];
-            for (int64_t uu = 0; uu < nu; ++uu) acc = fmaf(gk[uu * stride], ak[uu], acc);
+            for (int uu = 0; uu < nu; ++uu) acc = fmaf(gk[uu * stride], ak[uu], acc);
         }
         gb[r * d.S + f] = acc;
     }
@@ -118,30 +125,31 @@ __global__ void combine_group_kernel(const GroupParams p) {
     const int64_t g = blockIdx.x, b = blockIdx.y;
     const int64_t j0 = g * p.G;
     const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
-    const int64_t S = d.S;
-    for (int64_t e = threadIdx.x; e < (int64_t)cnt * S; e += blockDim.x) {
-        const int64_t jj = e / S, f = e % S;
-        gs[e] = p.in[(j0 + jj) * p.in_sj + b * p.in_sb + f];
+    const int S = d.S;
+    for (int jj = 0; jj < cnt; ++jj) {
+        const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
+        float* dst = gs + jj * S;
+        for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = src[f];
     }
     __syncthreads();
     for (int stride = 1; stride < cnt; stride <<= 1) {
         const int npairs = (cnt + 2 * stride - 1) / (2 * stride);
         for (int k = d.N; k >= 1; --k) {
-            const int64_t nw = d.pw[k];
-            for (int64_t e = threadIdx.x; e < (int64_t)npairs * nw; e += blockDim.x) {
-                const int pr = (int)(e / nw);
-                const int64_t w = e % nw;
+            const int nw = d.pw[k];
+            for (int e = threadIdx.x; e < npairs * nw; e += blockDim.x) {
+                const int pr = e / nw;
+                const int w = e - pr * nw;
                 const int left = pr * 2 * stride, right = left + stride;
                 if (right >= cnt) continue;
-                float* x = gs + (int64_t)left * S;
-                const float* y = gs + (int64_t)right * S;
+                float* x = gs + left * S;
+                const float* y = gs + right * S;
                 x[d.off[k] + w] = mul_coef(d, x, y, k, w);
             }
             __syncthreads();
         }
     }
     float* o = p.out + g * p.out_sj + b * p.out_sb;
-    for (int64_t f = threadIdx.x; f < S; f += blockDim.x) o[f] = gs[f];
+    for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = gs[f];
 }
 
 }  // namespace sigb200

@@ -8,13 +8,12 @@
 // BRACKETS = (psi o phi)^{-1} psi(log) as a sparse mat-vec with the exact integer
 // inverse built on the host; EXPAND = log itself.
 //
-// One CTA per signature row; x (float, as stored) and the H_n (double) live in shared memory.
-// The series cancels heavily at deep levels (at C=4, N=7 the float evaluation loses ~1e-4
-// relative at level 7 while the log is well conditioned in its input: ~1e-6), so the
-// arithmetic of K4/K5 is float64 with float32 inputs and outputs.  The work is
-// ~N*S FMAs per row (about 2-5% of the scan at the BASELINE shapes): a latency-bound epilogue,
-// not a roofline kernel.  The backward (K5) walks the Horner recursion in reverse and produces the
-// dense gradient w.r.t. the signature that seeds the reversible signature backward (K2).
+// One CTA (1024 threads) per signature row; x and the H_n live in shared memory.  The series
+// cancels heavily at deep levels (at C=4, N=7 a float evaluation loses ~1e-4 relative at level 7
+// while the log is well conditioned in its input: ~1e-6), so the forward (K4) computes in float64
+// with float32 inputs and outputs; the backward (K5) has no such cancellation and stays float32
+// (DESIGN.md "K4").
+// Index arithmetic is 32-bit; divisions by C use a precomputed magic multiplier.
 #pragma once
 #include "combine.cuh"
 
@@ -31,61 +30,101 @@ struct LogsigTables {
     const float* minvT_val;
 };
 
+// 32-bit level tables of one (C, N), built on the host
+struct LDims {
+    int C, N, S;
+    int pw[17];    // C^k
+    int off[18];   // flat offset of level k (1-based) in the S layout; off[N+1] = S
+    int hoff[18];  // offset of level m (0-based, scalar level 0 included) in an H array
+    uint32_t magic;  // n / C == __umulhi(n, magic) for n < 2^24
+};
+
+inline LDims make_ldims(int C, int N) {
+    LDims d{};
+    d.C = C;
+    d.N = N;
+    d.pw[0] = 1;
+    for (int k = 1; k <= 16; ++k) d.pw[k] = (k <= N + 1) ? d.pw[k - 1] * C : 0;
+    d.off[1] = 0;
+    for (int k = 1; k <= N; ++k) d.off[k + 1] = d.off[k] + d.pw[k];
+    d.S = d.off[N + 1];
+    d.hoff[0] = 0;
+    for (int m = 0; m <= N; ++m) d.hoff[m + 1] = d.hoff[m] + d.pw[m];
+    // magic = ceil(2^32 / C): floor(n * magic / 2^32) == floor(n / C) exactly for n < 2^32 / C
+    d.magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)C - 1) / (uint64_t)C);
+    return d;
+}
+
+__device__ __forceinline__ int divC(const LDims& d, int n) {
+    return (d.C == 1) ? n : (int)__umulhi((uint32_t)n, d.magic);
+}
+
+// level of flat coefficient f (1..N) -- at most N compares, no division
+__device__ __forceinline__ int lvl_of(const LDims& d, int f) {
+    int k = 1;
+    while (k < d.N && f >= d.off[k + 1]) ++k;
+    return k;
+}
+// level m of an index e into an H array (levels 0..)
+__device__ __forceinline__ int hlvl_of(const LDims& d, int e) {
+    int m = 0;
+    while (e >= d.hoff[m + 1]) ++m;
+    return m;
+}
+
+// (x H)_k[w] = sum_{i=1}^{k} x_i[w / C^(k-i)] H_{k-i}[w mod C^(k-i)]   (H given on levels 0..k-1)
+__device__ __forceinline__ double xh_coef(const LDims& d, const float* xs, const double* H, int k, int w) {
+    double acc = 0.0;
+    int u = w, v = 0, q = 1;  // i = k: prefix w, empty suffix
+    for (int i = k; i >= 1; --i) {
+        acc = fma((double)xs[d.off[i] + u], H[d.hoff[k - i] + v], acc);
+        const int u2 = divC(d, u);
+        v += (u - u2 * d.C) * q;
+        q *= d.C;
+        u = u2;
+    }
+    return acc;
+}
+
 struct LogsigParams {
-    TensorDims d;
+    LDims d;
     int mode;                     // 0 expand, 1 brackets, 2 words
     LogsigTables tb;
     int64_t rows;
     const float* sig;             // [rows, S]
     float* out;                   // fwd: [rows, w|S]
     const float* gout;            // bwd: [rows, w|S]
-    float* gsig;                  // bwd: [rows, S] output
-    float* glog_ws;               // bwd scratch [rows, S] (brackets/words)
+    float* gsig;                  // bwd: [rows, S] output (accumulated in place)
+    float* glog_ws;               // bwd scratch [rows, S]: dense dL/dlog (words / brackets)
 };
 
-__device__ __forceinline__ int64_t hoff(const TensorDims& d, int m) {  // levels 0..m-1 sizes
-    int64_t s = 0;
-    for (int j = 0; j < m; ++j) s += d.pw[j];
-    return s;
-}
+constexpr int LOGSIG_THREADS = 1024;
 
-// (x H)_k[w] = sum_{i=1}^{k} x_i[w / C^(k-i)] H_{k-i}[w mod C^(k-i)]   (H given on levels 0..k-1)
-__device__ __forceinline__ double xh_coef(const TensorDims& d, const float* xs, const double* H, int k, int64_t w) {
-    double acc = 0.0;
-    for (int i = 1; i <= k; ++i) {
-        const int64_t q = d.pw[k - i];
-        acc = fma((double)xs[d.off[i] + w / q], H[hoff(d, k - i) + w % q], acc);
-    }
-    return acc;
-}
-
-__global__ void logsig_fwd_kernel(const LogsigParams p) {
-    const TensorDims& d = p.d;
-    const int N = d.N;
-    const int64_t S = d.S;
+__global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_fwd_kernel(const LogsigParams p) {
+    const LDims& d = p.d;
+    const int N = d.N, S = d.S;
     const int64_t row = blockIdx.x;
     extern __shared__ __align__(16) double lsd[];
-    const int64_t HS = hoff(d, N);  // levels 0..N-1
+    const int HS = d.hoff[N];  // levels 0..N-1
     double* Ha = lsd;
     double* Hb = Ha + HS;
     float* xs = reinterpret_cast<float*>(Hb + HS);  // [S]
     float* psi = xs + S;                            // [w] (brackets only)
     const float* src = p.sig + row * S;
-    for (int64_t f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
+    for (int f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
     if (threadIdx.x == 0) Ha[0] = 1.0 / (double)N;
     __syncthreads();
     double* Hc = Ha;
     double* Hn = Hb;
     for (int n = N - 1; n >= 1; --n) {
         const int top = N - n;  // H_n on levels 0..top
-        for (int64_t e = threadIdx.x; e < hoff(d, top + 1); e += blockDim.x) {
+        for (int e = threadIdx.x; e < d.hoff[top + 1]; e += blockDim.x) {
             if (e == 0) {
                 Hn[0] = 1.0 / (double)n;
                 continue;
             }
-            int m = 1;
-            while (e >= hoff(d, m + 1)) ++m;
-            Hn[e] = -xh_coef(d, xs, Hc, m, e - hoff(d, m));
+            const int m = hlvl_of(d, e);
+            Hn[e] = -xh_coef(d, xs, Hc, m, e - d.hoff[m]);
         }
         __syncthreads();
         double* t = Hc;
@@ -95,16 +134,16 @@ __global__ void logsig_fwd_kernel(const LogsigParams p) {
     // log = x H_1
     if (p.mode == 0) {
         float* o = p.out + row * S;
-        for (int64_t f = threadIdx.x; f < S; f += blockDim.x) {
-            const int k = level_of(d, f);
+        for (int f = threadIdx.x; f < S; f += blockDim.x) {
+            const int k = lvl_of(d, f);
             o[f] = (float)xh_coef(d, xs, Hc, k, f - d.off[k]);
         }
         return;
     }
     float* o = p.out + row * p.tb.w;
     for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
-        const int64_t f = p.tb.lyn_idx[j];
-        const int k = level_of(d, f);
+        const int f = (int)p.tb.lyn_idx[j];
+        const int k = lvl_of(d, f);
         const double v = xh_coef(d, xs, Hc, k, f - d.off[k]);
         if (p.mode == 2) o[j] = (float)v;
         else psi[j] = (float)v;
@@ -126,48 +165,74 @@ __global__ void logsig_fwd_kernel(const LogsigParams p) {
 //                           gH1_m[v] = sum_i sum_u x_i[u] g_{i+m}[u v]          (m >= 1)
 //   H_n = c_n - x H_{n+1}:  gx_i[u] -= sum_m sum_v gHn_{i+m}[u v] H_{n+1},m[v];
 //                           gH{n+1}_m[v] = -sum_i sum_u x_i[u] gHn_{i+m}[u v]   (m >= 1)
-// Every thread owns a fixed set of gx coefficients across the steps (no races, fixed order).
-__global__ void logsig_bwd_kernel(const LogsigParams p) {
-    const TensorDims& d = p.d;
-    const int N = d.N;
-    const int64_t S = d.S;
+// float32 arithmetic (the backward has no cancellation problem: ~1e-5 measured vs the 5e-4 bar).
+// Every pass is a set of independent dot products of very different lengths (a level-1 coefficient
+// sums over most of the tensor, a top-level one over one term), so each pass flattens all its
+// outputs into one list of warp slots: short outputs take one lane each, long ones a group of up to
+// 32 lanes that split the inner index and combine with an xor-shuffle tree (fixed order:
+// deterministic).  gH is double-buffered so all levels of a pass are independent.  Each dL/dSig
+// coefficient has one owner and accumulates in place in the output row.
+__device__ __forceinline__ int group_for(int work) {
+    int G = 1;
+    while (G < 32 && G * 16 < work) G <<= 1;
+    return G;
+}
+
+__device__ __forceinline__ float group_sum(float v, int G) {
+    for (int m = G >> 1; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+
+__global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const LogsigParams p) {
+    const LDims& d = p.d;
+    const int N = d.N, S = d.S;
     const int64_t row = blockIdx.x;
-    extern __shared__ __align__(16) double lsd[];
-    const int64_t HS = hoff(d, N);
-    auto hb = [&](int n) -> int64_t {  // offset of H_n (levels 0..N-n) in Hall
-        int64_t s = 0;
-        for (int q = N; q > n; --q) s += hoff(d, N - q + 1);
+    extern __shared__ __align__(16) float lsf[];
+    const int HS = d.hoff[N];
+    auto hb = [&](int n) -> int {  // offset of H_n (levels 0..N-n); H_N first
+        int s = 0;
+        for (int q = N; q > n; --q) s += d.hoff[N - q + 1];
         return s;
     };
-    double* Hall = lsd;
-    double* gH = Hall + hb(0);                      // [HS] gradient of the current H_n (in place)
-    float* xs = reinterpret_cast<float*>(gH + HS);  // [S]
+    float* Hall = lsf;                 // all H_n
+    float* gHa = Hall + hb(0);         // [HS] dL/dH, double-buffered
+    float* gHb = gHa + HS;             // [HS]
+    float* xs = gHb + HS;              // [S]
     const float* src = p.sig + row * S;
-    for (int64_t f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
-    if (threadIdx.x == 0) Hall[hb(N)] = 1.0 / (double)N;
+    for (int f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
+    if (threadIdx.x == 0) Hall[hb(N)] = 1.0f / (float)N;
     __syncthreads();
     for (int n = N - 1; n >= 1; --n) {
         const int top = N - n;
-        double* Hn = Hall + hb(n);
-        const double* Hc = Hall + hb(n + 1);
-        for (int64_t e = threadIdx.x; e < hoff(d, top + 1); e += blockDim.x) {
+        float* Hn = Hall + hb(n);
+        const float* Hc = Hall + hb(n + 1);
+        for (int e = threadIdx.x; e < d.hoff[top + 1]; e += blockDim.x) {
             if (e == 0) {
-                Hn[0] = 1.0 / (double)n;
+                Hn[0] = 1.0f / (float)n;
                 continue;
             }
-            int m = 1;
-            while (e >= hoff(d, m + 1)) ++m;
-            Hn[e] = -xh_coef(d, xs, Hc, m, e - hoff(d, m));
+            const int m = hlvl_of(d, e);
+            const int w = e - d.hoff[m];
+            float acc = 0.0f;
+            int u = w, v = 0, q = 1;
+            for (int i = m; i >= 1; --i) {
+                acc = fmaf(xs[d.off[i] + u], Hc[d.hoff[m - i] + v], acc);
+                const int u2 = divC(d, u);
+                v += (u - u2 * d.C) * q;
+                q *= d.C;
+                u = u2;
+            }
+            Hn[e] = -acc;
         }
         __syncthreads();
     }
-    // dense dL/dlog (float32 in the workspace for words/brackets)
-    const float* g;
+    // dense dL/dlog
+    const float* gl;
     if (p.mode == 0) {
-        g = p.gout + row * S;
+        gl = p.gout + row * S;
     } else {
         float* gw = p.glog_ws + row * S;
-        for (int64_t f = threadIdx.x; f < S; f += blockDim.x) gw[f] = 0.0f;
+        for (int f = threadIdx.x; f < S; f += blockDim.x) gw[f] = 0.0f;
         __syncthreads();
         const float* go = p.gout + row * p.tb.w;
         for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
@@ -179,91 +244,113 @@ __global__ void logsig_bwd_kernel(const LogsigParams p) {
                 for (int e = p.tb.minvT_rowptr[j]; e < p.tb.minvT_rowptr[j + 1]; ++e)
                     v = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], v);
             }
-            gw[p.tb.lyn_idx[j]] = (float)v;
+            gw[(int)p.tb.lyn_idx[j]] = (float)v;
         }
-        __syncthreads();
-        g = gw;
+        gl = gw;
     }
     float* gx = p.gsig + row * S;
-    // step A: log = x H_1 (H_1 on levels 0..N-1)
-    {
-        const double* H1 = Hall + hb(1);
-        for (int64_t f = threadIdx.x; f < S; f += blockDim.x) {
-            const int i = level_of(d, f);
-            const int64_t u = f - d.off[i];
-            double acc = 0.0;
-            for (int m = 0; m <= N - i; ++m) {
-                const int64_t nv = d.pw[m];
-                const float* gk = g + d.off[i + m] + u * nv;
-                const double* hm = H1 + hoff(d, m);
-                for (int64_t v = 0; v < nv; ++v) acc = fma((double)gk[v], hm[v], acc);
-            }
-            gx[f] = (float)acc;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+
+    // gx_i[u] (+)= sgn * sum_{m=0}^{top-i} sum_v src_{i+m}[u C^m + v] * Hm[v],  i = 1..top
+    // src(level k, idx) = gl[off[k] + idx] (step A) or gHs[hoff[k] + idx]
+    auto gx_pass = [&](int top, const float* gHs, const float* Hm, float sgn, bool init) {
+        // warp slots: level i needs ceil(C^i / (32 / G_i)) of them
+        int total = 0;
+        for (int i = 1; i <= top; ++i) {
+            const int G = group_for(d.hoff[top - i + 1]);
+            total += (d.pw[i] * G + 31) / 32;
         }
-        for (int64_t e = threadIdx.x; e < HS; e += blockDim.x) {
-            if (e == 0) continue;
-            int m = 1;
-            while (e >= hoff(d, m + 1)) ++m;
-            const int64_t v = e - hoff(d, m);
-            double acc = 0.0;
-            for (int i = 1; i <= N - m; ++i) {
-                const int64_t nu = d.pw[i];
-                const float* gk = g + d.off[i + m] + v;
-                const float* xi = xs + d.off[i];
-                for (int64_t u = 0; u < nu; ++u) acc = fma((double)xi[u], (double)gk[u * d.pw[m]], acc);
+        for (int slot = warp; slot < total; slot += nwarps) {
+            int i = 1, base = slot, G = 1;
+            for (;; ++i) {
+                G = group_for(d.hoff[top - i + 1]);
+                const int ns = (d.pw[i] * G + 31) / 32;
+                if (base < ns) break;
+                base -= ns;
             }
-            gH[e] = acc;
-        }
-        __syncthreads();
-    }
-    for (int n = 1; n <= N - 1; ++n) {
-        const int top = N - n;  // gH = dL/dH_n on levels 1..top
-        const double* Hnext = Hall + hb(n + 1);  // levels 0..top-1
-        for (int64_t f = threadIdx.x; f < d.off[top + 1]; f += blockDim.x) {
-            const int i = level_of(d, f);
-            const int64_t u = f - d.off[i];
-            double acc = 0.0;
-            for (int m = 0; m <= top - i; ++m) {
-                const int64_t nv = d.pw[m];
-                const double* gk = gH + hoff(d, i + m) + u * nv;
-                const double* hm = Hnext + hoff(d, m);
-                for (int64_t v = 0; v < nv; ++v) acc = fma(gk[v], hm[v], acc);
-            }
-            gx[f] = (float)((double)gx[f] - acc);
-        }
-        __syncthreads();
-        // dL/dH_{n+1} in place, level by level upward: level m reads only levels > m
-        if (n <= N - 2) {
-            for (int m = 1; m <= top - 1; ++m) {
-                for (int64_t v = threadIdx.x; v < d.pw[m]; v += blockDim.x) {
-                    double acc = 0.0;
-                    for (int i = 1; i <= top - m; ++i) {
-                        const int64_t nu = d.pw[i];
-                        const double* gk = gH + hoff(d, i + m) + v;
-                        const float* xi = xs + d.off[i];
-                        for (int64_t u = 0; u < nu; ++u) acc = fma((double)xi[u], gk[u * d.pw[m]], acc);
+            const int work = d.hoff[top - i + 1];
+            const int u = base * (32 / G) + lane / G, gq = lane % G;
+            float acc = 0.0f;
+            if (u < d.pw[i]) {
+                int m = 0, mend = 1;
+                for (int t = gq; t < work; t += G) {
+                    while (t >= mend) {
+                        ++m;
+                        mend = d.hoff[m + 1];
                     }
-                    gH[hoff(d, m) + v] = -acc;
+                    const int idx = u * d.pw[m] + (t - d.hoff[m]);
+                    const float g = gHs ? gHs[d.hoff[i + m] + idx] : gl[d.off[i + m] + idx];
+                    acc = fmaf(g, Hm[t], acc);
                 }
-                __syncthreads();
+            }
+            acc = group_sum(acc, G);
+            if (gq == 0 && u < d.pw[i]) {
+                float* dst = &gx[d.off[i] + u];
+                *dst = init ? sgn * acc : fmaf(sgn, acc, *dst);
             }
         }
+    };
+    // gHo_m[v] = sgn * sum_{i=1}^{top-m} sum_u x_i[u] src_{i+m}[u C^m + v],  m = 1..top-1
+    auto gh_pass = [&](int top, const float* gHs, float* gHo, float sgn) {
+        int total = 0;
+        for (int m = 1; m <= top - 1; ++m) {
+            const int G = group_for(d.off[top - m + 1]);
+            total += (d.pw[m] * G + 31) / 32;
+        }
+        for (int slot = warp; slot < total; slot += nwarps) {
+            int m = 1, base = slot, G = 1;
+            for (;; ++m) {
+                G = group_for(d.off[top - m + 1]);
+                const int ns = (d.pw[m] * G + 31) / 32;
+                if (base < ns) break;
+                base -= ns;
+            }
+            const int work = d.off[top - m + 1];  // sum_{i=1}^{top-m} C^i
+            const int v = base * (32 / G) + lane / G, gq = lane % G;
+            float acc = 0.0f;
+            if (v < d.pw[m]) {
+                int i = 1, iend = d.off[2];
+                for (int t = gq; t < work; t += G) {
+                    while (t >= iend) {
+                        ++i;
+                        iend = d.off[i + 1];
+                    }
+                    const int idx = (t - d.off[i]) * d.pw[m] + v;
+                    const float g = gHs ? gHs[d.hoff[i + m] + idx] : gl[d.off[i + m] + idx];
+                    acc = fmaf(xs[t], g, acc);  // xs[off[i] + u] == xs[t]
+                }
+            }
+            acc = group_sum(acc, G);
+            if (gq == 0 && v < d.pw[m]) gHo[d.hoff[m] + v] = sgn * acc;
+        }
+    };
+    // step A: log = x H_1 (H_1 on levels 0..N-1)
+    gx_pass(N, nullptr, Hall + hb(1), 1.0f, true);
+    gh_pass(N, nullptr, gHa, 1.0f);
+    __syncthreads();
+    float* gc = gHa;
+    float* gn = gHb;
+    for (int n = 1; n <= N - 1; ++n) {
+        const int top = N - n;  // gc = dL/dH_n on levels 1..top
+        gx_pass(top, gc, Hall + hb(n + 1), -1.0f, false);
+        if (n <= N - 2) gh_pass(top, gc, gn, -1.0f);
+        __syncthreads();
+        float* t = gc;
+        gc = gn;
+        gn = t;
     }
 }
 
-inline size_t logsig_fwd_smem(const TensorDims& d, int w, bool brackets) {
-    int64_t HS = 0;
-    for (int j = 0; j < d.N; ++j) HS += d.pw[j];
-    return (size_t)(2 * HS) * sizeof(double) + (size_t)(d.S + (brackets ? w : 0)) * sizeof(float);
+inline size_t logsig_fwd_smem(const LDims& d, int w, bool brackets) {
+    return (size_t)(2 * d.hoff[d.N]) * sizeof(double) + (size_t)(d.S + (brackets ? w : 0)) * sizeof(float);
 }
 
-inline size_t logsig_bwd_smem(const TensorDims& d) {
-    int64_t HS = 0;
-    for (int j = 0; j < d.N; ++j) HS += d.pw[j];
-    int64_t hall = 0;
-    for (int n = 1; n <= d.N; ++n)
-        for (int j = 0; j <= d.N - n; ++j) hall += d.pw[j];
-    return (size_t)(hall + HS) * sizeof(double) + (size_t)d.S * sizeof(float);
+inline size_t logsig_bwd_smem(const LDims& d) {
+    int hall = 0;
+    for (int n = 1; n <= d.N; ++n) hall += d.hoff[d.N - n + 1];
+    return (size_t)(hall + 2 * d.hoff[d.N] + d.S) * sizeof(float);
 }
 
 }  // namespace sigb200

@@ -168,29 +168,39 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
 
     for (int64_t t0 = 0; t0 < prm.chunk_len; t0 += T) {
         __syncthreads();
-        // ---- stage increments z = X[s+1] - X[s] of this tile for the CTA's units
-        const int nel = nu * T * C;
-        for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-            const int c = e % C;
-            const int t = (e / C) % T;
-            const int uu = e / (C * T);
+        // ---- stage the increments z = X[s+1] - X[s] of this tile for the CTA's units.  Per unit
+        // the points are one contiguous run of the path (coalesced, independent loads unrolled for
+        // memory-level parallelism); index math is 32-bit inside the tile.
+        for (int uu = 0; uu < nu; ++uu) {
             const int64_t un = unit0 + uu;
-            float zv = 0.0f;
+            int cnt = 0;          // valid increments of this unit in this tile
+            int64_t rowbase = 0;  // element offset of augmented point (s - has_bp) of the tile start
+            int64_t bb = 0;
             if (un < prm.n_units) {
-                const int64_t bb = un / prm.n_chunks, jj = un % prm.n_chunks;
-                const int64_t s = jj * prm.chunk_len + t0 + t;
-                if (t0 + t < prm.chunk_len && s < prm.M) {
-                    const float* xr = prm.path + bb * prm.L * C;
-                    // augmented point r: r == 0 is the basepoint when one is given
-                    const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
-                    const float x1 = xr[r1 * C + c];
+                bb = un / prm.n_chunks;
+                const int64_t jj = un - bb * prm.n_chunks;
+                const int64_t s = jj * prm.chunk_len + t0;
+                const int64_t ulen = (prm.chunk_len < prm.M - jj * prm.chunk_len ? prm.chunk_len
+                                                                                  : prm.M - jj * prm.chunk_len);
+                cnt = (int)(ulen - t0 < T ? (ulen - t0 > 0 ? ulen - t0 : 0) : T);
+                rowbase = (bb * prm.L + (s - has_bp)) * C;
+            }
+            float* zu = zs + (size_t)uu * T * C;
+            const float* xb = prm.path;
+#pragma unroll 4
+            for (int i = threadIdx.x; i < T * C; i += blockDim.x) {
+                const int t = i / C, c = i - (i / C) * C;
+                float zv = 0.0f;
+                if (t < cnt) {
+                    const int64_t g0 = rowbase + i;  // point (s + t - has_bp), channel c
+                    const float x1 = __ldg(xb + g0 + C);
                     float x0;
-                    if (r0 >= 0) x0 = xr[r0 * C + c];
+                    if (g0 >= bb * prm.L * C) x0 = __ldg(xb + g0);
                     else x0 = (prm.bp_mode == 2) ? prm.basepoint[bb * C + c] : 0.0f;
                     zv = x1 - x0;
                 }
+                zu[t * C + zswz(C, c)] = zv;  // pair-swapped staging when enabled (see zswz)
             }
-            zs[e - c + zswz(C, c)] = zv;  // pair-swapped staging (see zswz)
         }
         __syncthreads();
         const int tl = (int)((int64_t)T < prm.chunk_len - t0 ? (int64_t)T : prm.chunk_len - t0);
@@ -224,9 +234,21 @@ template <class SH>
 cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     FwdParams prm = prm_in;
     const int64_t threads = prm.n_units * (int64_t)SH::CP;
+    // CTA size: units never communicate, so any size works.  Small problems are spread over more
+    // SMs (latency-bound, e.g. BASELINE config c1); otherwise pick the size whose CTA count divides
+    // most evenly over the 148 SMs (a path of units assigned to 2 CTAs on some SMs and 1 on others
+    // would leave SMs idle -- c3 lost 31% that way), preferring larger CTAs on ties.
     int bd = 512;
-    // small problems: spread over more SMs (latency-bound, e.g. BASELINE config c1)
-    while (bd > 32 && (threads + bd - 1) / bd < 148) bd /= 2;
+    double best = -1.0;
+    for (int cand = 512; cand >= 32; cand /= 2) {
+        const int64_t ctas = (threads + cand - 1) / cand;
+        const int64_t waves = (ctas + 147) / 148;
+        const double eff = (double)ctas / (double)(waves * 148);  // busiest SM vs average
+        if (eff > best + 1e-6) {
+            best = eff;
+            bd = cand;
+        }
+    }
     const int64_t grid = (threads + bd - 1) / bd;
     const int nu = (int)((bd - 1) / SH::CP + 2);  // max units touched by one CTA
     int tile = (int)(prm.chunk_len < 256 ? prm.chunk_len : 256);
