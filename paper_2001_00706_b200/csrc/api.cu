@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/sig.h"
+#define SIG_DEFINE_COMBINE_KERNELS
 #include "combine.cuh"
 #include "logsig.cuh"
 #include "lyndon.h"
@@ -64,13 +65,16 @@ struct FwdPlan {
     FwdLaunch launch;
     int64_t M, n_chunks, chunk_len;
     int G;                  // group size of the chunk fold
+    int upc;                // chunks folded inside each scan CTA (0: none)
+    int64_t n_parts;        // partial signatures per path left for the fold kernels
     int64_t fold_levels[40];
     int n_fold;             // number of fold launches (after the scan)
     size_t ws_bytes;
 };
 
 int group_size_for(int64_t S) {
-    int G = 32;
+    // small groups: many CTAs, few loads per thread (the fold is latency-bound, not FLOP-bound)
+    int G = 8;
     while (G > 2 && (size_t)G * S * sizeof(float) > 200 * 1024) G >>= 1;
     if ((size_t)G * S * sizeof(float) > 200 * 1024) return 0;  // pairwise in global memory
     return G;
@@ -120,14 +124,32 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
         pl.P = ks->pf1;
         pl.launch = ks->fwd1;
     }
+    pl.upc = 0;
+    if (pl.n_chunks > 1) {
+        // group chunks so that each scan CTA folds upc consecutive chunks of one path itself
+        const int cp = (int)sigb200::ipow(C, pl.P);
+        int upc = cp <= 512 ? 512 / cp : 0;
+        if (upc > 32) upc = 32;
+        while (upc >= 2 && (size_t)upc * S * sizeof(float) > 200 * 1024) --upc;
+        if (upc >= 2) {
+            pl.upc = upc;
+            // one CTA per group of upc chunks: make the CTA count a whole number of waves
+            int64_t groups = (B * pl.n_chunks + upc - 1) / upc;
+            groups = (groups + 147) / 148 * 148;
+            int64_t per_path = (groups + B - 1) / B;
+            if (per_path * upc > M) per_path = M / upc > 0 ? M / upc : 1;
+            pl.n_chunks = per_path * upc;
+        }
+    }
     pl.chunk_len = (M + pl.n_chunks - 1) / pl.n_chunks;
-    pl.n_chunks = (M + pl.chunk_len - 1) / pl.chunk_len;
+    if (pl.upc == 0) pl.n_chunks = (M + pl.chunk_len - 1) / pl.chunk_len;
+    pl.n_parts = pl.upc > 0 ? pl.n_chunks / pl.upc : pl.n_chunks;
     size_t elems = 0;
     pl.n_fold = 0;
     pl.G = 0;
     if (pl.n_chunks > 1) {
-        plan_fold(pl.n_chunks, S, B, pl.G, pl.fold_levels, pl.n_fold, elems);
-        elems += (size_t)pl.n_chunks * B * S;  // the chunk signatures themselves
+        if (pl.n_parts > 1) plan_fold(pl.n_parts, S, B, pl.G, pl.fold_levels, pl.n_fold, elems);
+        elems += (size_t)pl.n_parts * B * S;  // the (partial) chunk signatures themselves
     }
     pl.ws_bytes = elems * sizeof(float);
     return ok();
@@ -178,7 +200,7 @@ cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_
                 if (e != cudaSuccess) return e;
             }
             dim3 grid((unsigned)ng, (unsigned)B);
-            combine_group_kernel<<<grid, 256, smem, st>>>(gp);
+            combine_group_kernel<<<grid, 512, smem, st>>>(gp);
             count_launch();
         } else {
             // pairwise in global memory: dst(g) = cur(2g) [x] cur(2g+1)
@@ -229,15 +251,19 @@ sig_status_t run_signature(const float* path, int64_t B, int64_t L, int64_t C, i
     prm.chunk_len = pl.chunk_len;
     prm.n_chunks = pl.n_chunks;
     prm.n_units = B * pl.n_chunks;
-    float* units = (pl.n_chunks > 1) ? static_cast<float*>(ws) : out;
+    prm.upc = pl.upc;
+    prm.dims = d;
+    float* units = (pl.n_chunks > 1 && pl.n_parts > 1) ? static_cast<float*>(ws) : out;
     prm.out = units;
     cudaError_t e = pl.launch(prm, s);
+    if (e == cudaErrorInvalidConfiguration)
+        return fail(SIG_ERR_UNSUPPORTED, "scan configuration exceeds the shared memory of one CTA");
     if (e != cudaSuccess) return cuda_status(e, "signature scan launch");
     count_launch();
-    if (pl.n_chunks > 1) {
-        // unit (b, j) at units + (b*n_chunks + j)*S  ->  element (j, b): sj = S, sb = n_chunks*S
-        float* fold_ws = units + (size_t)pl.n_chunks * B * d.S;
-        e = launch_fold(d, units, d.S, pl.n_chunks * d.S, pl.n_chunks, B, out, fold_ws, s);
+    if (pl.n_chunks > 1 && pl.n_parts > 1) {
+        // part (b, j) at units + (b*n_parts + j)*S  ->  element (j, b): sj = S, sb = n_parts*S
+        float* fold_ws = units + (size_t)pl.n_parts * B * d.S;
+        e = launch_fold(d, units, d.S, pl.n_parts * d.S, pl.n_parts, B, out, fold_ws, s);
         if (e != cudaSuccess) return cuda_status(e, "chunk fold launch");
     }
     return ok();

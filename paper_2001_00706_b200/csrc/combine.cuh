@@ -60,6 +60,7 @@ __device__ __forceinline__ float mul_coef(const TensorDims& d, const float* a, c
     return acc;
 }
 
+#ifdef SIG_DEFINE_COMBINE_KERNELS  // defined only by api.cu, the one TU that launches them
 // ---------------------------------------------------------------- pairwise, batched
 // row r: out + r*so = (a + r*sa) [x] (b + r*sb)
 __global__ void combine_pair_kernel(const TensorDims d, const float* __restrict__ a, int64_t sa,
@@ -108,6 +109,8 @@ __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restr
     }
 }
 
+#endif  // SIG_DEFINE_COMBINE_KERNELS
+
 // ---------------------------------------------------------------- ordered group fold in smem
 struct GroupParams {
     TensorDims d;
@@ -119,19 +122,11 @@ struct GroupParams {
     int64_t out_sj, out_sb;  // group result (g, b) at out + g*out_sj + b*out_sb
 };
 
-__global__ void combine_group_kernel(const GroupParams p) {
-    extern __shared__ float gs[];  // [G][S]
-    const TensorDims& d = p.d;
-    const int64_t g = blockIdx.x, b = blockIdx.y;
-    const int64_t j0 = g * p.G;
-    const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
+// In-place ordered binary-tree product of cnt signatures gs[0..cnt) (S floats each) held in
+// shared memory by the whole CTA; the result ends in gs[0].  Level by level, top-down: a level-k
+// update of the left operand reads only its levels < k and its own coefficient.
+__device__ __forceinline__ void block_tree_combine(float* gs, int cnt, const TensorDims& d) {
     const int S = d.S;
-    for (int jj = 0; jj < cnt; ++jj) {
-        const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
-        float* dst = gs + jj * S;
-        for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = src[f];
-    }
-    __syncthreads();
     for (int stride = 1; stride < cnt; stride <<= 1) {
         const int npairs = (cnt + 2 * stride - 1) / (2 * stride);
         for (int k = d.N; k >= 1; --k) {
@@ -148,8 +143,28 @@ __global__ void combine_group_kernel(const GroupParams p) {
             __syncthreads();
         }
     }
+}
+
+#ifdef SIG_DEFINE_COMBINE_KERNELS
+__global__ void combine_group_kernel(const GroupParams p) {
+    extern __shared__ float gs[];  // [G][S]
+    const TensorDims& d = p.d;
+    const int64_t g = blockIdx.x, b = blockIdx.y;
+    const int64_t j0 = g * p.G;
+    const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
+    const int S = d.S;
+    for (int jj = 0; jj < cnt; ++jj) {
+        const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
+        float* dst = gs + jj * S;
+#pragma unroll 4
+        for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = __ldg(src + f);
+    }
+    __syncthreads();
+    block_tree_combine(gs, cnt, d);
     float* o = p.out + g * p.out_sj + b * p.out_sb;
     for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = gs[f];
 }
+
+#endif  // SIG_DEFINE_COMBINE_KERNELS
 
 }  // namespace sigb200

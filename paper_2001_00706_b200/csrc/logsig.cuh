@@ -253,36 +253,41 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const Log
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 
+    // Work lists: level l of a pass needs ns[l] warp slots of (32 / G[l]) outputs each.
+    __shared__ int s_G[17], s_ns[17];
+    auto plan_pass = [&](int lo, int hi, bool gx_kind, int top) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int l = lo; l <= hi; ++l) {
+                const int work = gx_kind ? d.hoff[top - l + 1] : d.off[top - l + 1];
+                const int G = group_for(work);
+                s_G[l] = G;
+                s_ns[l] = (d.pw[l] * G + 31) / 32;
+            }
+        }
+        __syncthreads();
+    };
     // gx_i[u] (+)= sgn * sum_{m=0}^{top-i} sum_v src_{i+m}[u C^m + v] * Hm[v],  i = 1..top
     // src(level k, idx) = gl[off[k] + idx] (step A) or gHs[hoff[k] + idx]
     auto gx_pass = [&](int top, const float* gHs, const float* Hm, float sgn, bool init) {
-        // warp slots: level i needs ceil(C^i / (32 / G_i)) of them
+        plan_pass(1, top, true, top);
         int total = 0;
-        for (int i = 1; i <= top; ++i) {
-            const int G = group_for(d.hoff[top - i + 1]);
-            total += (d.pw[i] * G + 31) / 32;
-        }
+        for (int i = 1; i <= top; ++i) total += s_ns[i];
         for (int slot = warp; slot < total; slot += nwarps) {
-            int i = 1, base = slot, G = 1;
-            for (;; ++i) {
-                G = group_for(d.hoff[top - i + 1]);
-                const int ns = (d.pw[i] * G + 31) / 32;
-                if (base < ns) break;
-                base -= ns;
+            int i = 1, base = slot;
+            while (base >= s_ns[i]) {
+                base -= s_ns[i];
+                ++i;
             }
-            const int work = d.hoff[top - i + 1];
+            const int G = s_G[i];
             const int u = base * (32 / G) + lane / G, gq = lane % G;
             float acc = 0.0f;
             if (u < d.pw[i]) {
-                int m = 0, mend = 1;
-                for (int t = gq; t < work; t += G) {
-                    while (t >= mend) {
-                        ++m;
-                        mend = d.hoff[m + 1];
-                    }
-                    const int idx = u * d.pw[m] + (t - d.hoff[m]);
-                    const float g = gHs ? gHs[d.hoff[i + m] + idx] : gl[d.off[i + m] + idx];
-                    acc = fmaf(g, Hm[t], acc);
+                for (int m = 0; m <= top - i; ++m) {
+                    const int nv = d.pw[m];
+                    const float* srow = gHs ? gHs + d.hoff[i + m] + u * nv : gl + d.off[i + m] + u * nv;
+                    const float* hrow = Hm + d.hoff[m];
+                    for (int v = gq; v < nv; v += G) acc = fmaf(srow[v], hrow[v], acc);
                 }
             }
             acc = group_sum(acc, G);
@@ -294,32 +299,26 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const Log
     };
     // gHo_m[v] = sgn * sum_{i=1}^{top-m} sum_u x_i[u] src_{i+m}[u C^m + v],  m = 1..top-1
     auto gh_pass = [&](int top, const float* gHs, float* gHo, float sgn) {
+        if (top < 2) return;
+        plan_pass(1, top - 1, false, top);
         int total = 0;
-        for (int m = 1; m <= top - 1; ++m) {
-            const int G = group_for(d.off[top - m + 1]);
-            total += (d.pw[m] * G + 31) / 32;
-        }
+        for (int m = 1; m <= top - 1; ++m) total += s_ns[m];
         for (int slot = warp; slot < total; slot += nwarps) {
-            int m = 1, base = slot, G = 1;
-            for (;; ++m) {
-                G = group_for(d.off[top - m + 1]);
-                const int ns = (d.pw[m] * G + 31) / 32;
-                if (base < ns) break;
-                base -= ns;
+            int m = 1, base = slot;
+            while (base >= s_ns[m]) {
+                base -= s_ns[m];
+                ++m;
             }
-            const int work = d.off[top - m + 1];  // sum_{i=1}^{top-m} C^i
+            const int G = s_G[m];
             const int v = base * (32 / G) + lane / G, gq = lane % G;
             float acc = 0.0f;
             if (v < d.pw[m]) {
-                int i = 1, iend = d.off[2];
-                for (int t = gq; t < work; t += G) {
-                    while (t >= iend) {
-                        ++i;
-                        iend = d.off[i + 1];
-                    }
-                    const int idx = (t - d.off[i]) * d.pw[m] + v;
-                    const float g = gHs ? gHs[d.hoff[i + m] + idx] : gl[d.off[i + m] + idx];
-                    acc = fmaf(xs[t], g, acc);  // xs[off[i] + u] == xs[t]
+                const int stride = d.pw[m];
+                for (int i = 1; i <= top - m; ++i) {
+                    const int nu = d.pw[i];
+                    const float* xrow = xs + d.off[i];
+                    const float* srow = gHs ? gHs + d.hoff[i + m] + v : gl + d.off[i + m] + v;
+                    for (int u = gq; u < nu; u += G) acc = fmaf(xrow[u], srow[u * stride], acc);
                 }
             }
             acc = group_sum(acc, G);

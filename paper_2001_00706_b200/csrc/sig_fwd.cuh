@@ -14,6 +14,7 @@
 // chunk of one path ("splitting the computation up into chunks"); chunk results are
 // folded afterwards by the combine kernels (K3).
 #pragma once
+#include "combine.cuh"
 #include "sig_common.cuh"
 
 namespace sigb200 {
@@ -29,7 +30,10 @@ struct FwdParams {
     int64_t n_chunks;        // units per path (stream => 1)
     int64_t n_units;         // B * n_chunks
     int tile;                // increments staged per tile
-    float* out;              // stream: [B, M, S]; else unit u -> out + u * S
+    int upc;                 // > 0: grouped chunks -- each CTA holds upc consecutive chunks of one
+                             //      path and writes their ordered product to out + (u / upc) * S
+    TensorDims dims;         // level tables for the in-CTA fold (upc > 0)
+    float* out;              // stream: [B, M, S]; upc = 0: unit u -> out + u * S
 };
 
 // Depth-first walk of the thread's word tree for the level-K Horner chain (eq-fusedterm):
@@ -227,6 +231,18 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
             }
         }
     }
+    if (prm.upc > 0) {
+        // grouped time chunks: this CTA's units are consecutive chunks of one path; fold
+        // their signatures in time order in shared memory (Chen's identity, eq-grouplike) and write
+        // one partial product.  Units past the end hold the identity (zero state).
+        __syncthreads();
+        store_state<SH, false>(zs + (size_t)ul * SH::S, prefix, own, low);
+        __syncthreads();
+        block_tree_combine(zs, nu, prm.dims);
+        float* o = prm.out + (size_t)blockIdx.x * SH::S;
+        for (int f = threadIdx.x; f < (int)SH::S; f += blockDim.x) o[f] = zs[f];
+        return;
+    }
     if (valid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
 }
 
@@ -234,27 +250,38 @@ template <class SH>
 cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     FwdParams prm = prm_in;
     const int64_t threads = prm.n_units * (int64_t)SH::CP;
-    // CTA size: units never communicate, so any size works.  Small problems are spread over more
-    // SMs (latency-bound, e.g. BASELINE config c1); otherwise pick the size whose CTA count divides
-    // most evenly over the 148 SMs (a path of units assigned to 2 CTAs on some SMs and 1 on others
-    // would leave SMs idle -- c3 lost 31% that way), preferring larger CTAs on ties.
     int bd = 512;
-    double best = -1.0;
-    for (int cand = 512; cand >= 32; cand /= 2) {
-        const int64_t ctas = (threads + cand - 1) / cand;
-        const int64_t waves = (ctas + 147) / 148;
-        const double eff = (double)ctas / (double)(waves * 148);  // busiest SM vs average
-        if (eff > best + 1e-6) {
-            best = eff;
-            bd = cand;
+    if (prm.upc > 0) {
+        // grouped chunks: a CTA is exactly upc whole units (no unit straddles two CTAs)
+        bd = prm.upc * SH::CP;
+    } else {
+        // CTA size: units never communicate, so any size works.  Small problems are spread over
+        // more SMs (latency-bound, e.g. BASELINE config c1); otherwise pick the size whose CTA count
+        // divides most evenly over the 148 SMs (c3 lost 31% to SMs holding 2 CTAs next to SMs
+        // holding 1), preferring larger CTAs on ties.
+        double best = -1.0;
+        for (int cand = 512; cand >= 32; cand /= 2) {
+            const int64_t ctas = (threads + cand - 1) / cand;
+            const int64_t waves = (ctas + 147) / 148;
+            const double eff = (double)ctas / (double)(waves * 148);  // average vs busiest SM
+            if (eff > best + 1e-6) {
+                best = eff;
+                bd = cand;
+            }
         }
     }
     const int64_t grid = (threads + bd - 1) / bd;
-    const int nu = (int)((bd - 1) / SH::CP + 2);  // max units touched by one CTA
+    const int nu = (prm.upc > 0) ? prm.upc : (int)((bd - 1) / SH::CP + 2);  // max units touched by one CTA
     int tile = (int)(prm.chunk_len < 256 ? prm.chunk_len : 256);
     while (tile > 8 && (size_t)nu * tile * SH::C * 4 > 48 * 1024) tile /= 2;
     prm.tile = tile;
-    const size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
+    size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
+    if (prm.upc > 0 && (size_t)nu * SH::S * sizeof(float) > smem) smem = (size_t)nu * SH::S * sizeof(float);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(sig_fwd_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     sig_fwd_kernel<SH><<<(unsigned)grid, bd, smem, st>>>(prm);
     return cudaGetLastError();
 }
