@@ -30,8 +30,6 @@ struct FwdParams {
     int64_t n_chunks;        // units per path (stream => 1)
     int64_t n_units;         // B * n_chunks
     int tile;                // increments staged per tile
-    int cpad;                // threads per unit: CP, or CP rounded up to whole warps (stream mode)
-    int nu_max;              // staging rows per CTA (shared-memory layout, set by the launcher)
     int upc;                 // > 0: grouped chunks -- each CTA holds upc consecutive chunks of one
                              //      path and writes their ordered product to out + (u / upc) * S
     TensorDims dims;         // level tables for the in-CTA fold (upc > 0)
@@ -142,65 +140,16 @@ __device__ __forceinline__ void store_state(float* row, int prefix, const float 
     });
 }
 
-// Stream mode with units padded to whole warps: the 32 lanes of a warp own 32 consecutive prefixes
-// of one path, i.e. one contiguous segment per level of the output row.  The warp stages its
-// lanes' blocks in shared memory (odd row stride: conflict-free) and writes each segment with
-// consecutive lanes on consecutive words: full 32-byte sectors, one coalesced store per 32
-// floats, and the state registers are released as soon as the STS has read them.
-template <class SH>
-struct WarpStage {
-    __host__ __device__ static constexpr int pstride(int k) { return SH::own(k) | 1; }
-    __host__ __device__ static constexpr int seg(int k) {  // offset of level k's staging area
-        int s = 0;
-        for (int j = SH::K0; j < k; ++j) s += 32 * pstride(j);
-        return s;
-    }
-    static constexpr int FLOATS = seg(SH::N + 1);  // per warp
-};
-
-template <class SH>
-__device__ __forceinline__ void store_state_warp(float* row, int prefix, int lane, bool pvalid, float* wb,
-                                                 const float (&own)[SH::OWN], const float (&low)[SH::LOWA]) {
-    using WS = WarpStage<SH>;
-    const int p0 = prefix - lane;
-    const int nval = (SH::CP - p0) < 32 ? (SH::CP - p0) : 32;
-    static_for<SH::K0, SH::N + 1>([&](auto kc) {
-        constexpr int k = decltype(kc)::value;
-#pragma unroll
-        for (int i = 0; i < SH::own(k); ++i) wb[WS::seg(k) + lane * WS::pstride(k) + i] = own[SH::own_off(k) + i];
-    });
-    __syncwarp();
-    static_for<SH::K0, SH::N + 1>([&](auto kc) {
-        constexpr int k = decltype(kc)::value;
-        constexpr int ok = SH::own(k);
-        float* g = row + SH::lvl_off(k) + (int64_t)p0 * ok;
-        const int n = nval * ok;
-        for (int idx = lane; idx < n; idx += 32) {
-            const int l = idx / ok, i = idx - (idx / ok) * ok;
-            __stcs(g + idx, wb[WS::seg(k) + l * WS::pstride(k) + i]);
-        }
-    });
-    static_for<1, SH::P>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        constexpr int tail = (int)ipow(SH::C, SH::P - i);
-        if (pvalid && prefix % tail == 0) __stcs(row + SH::lvl_off(i) + prefix / tail, low[i]);
-    });
-    __syncwarp();
-}
-
 template <class SH>
 __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     constexpr int C = SH::C;
     extern __shared__ float zs[];  // [units in CTA][tile][C]
     const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
     const int64_t gt = g0 + threadIdx.x;
-    const int cpad = prm.cpad;
-    const int64_t unit = gt / cpad;
-    const int praw = (int)(gt % cpad);
-    const bool pvalid = praw < SH::CP;              // lanes padding a unit to whole warps
-    const int prefix = pvalid ? praw : SH::CP - 1;
-    const int64_t unit0 = g0 / cpad;
-    const int64_t unit1 = (g0 + blockDim.x - 1) / cpad;
+    const int64_t unit = gt / SH::CP;
+    const int prefix = (int)(gt % SH::CP);
+    const int64_t unit0 = g0 / SH::CP;
+    const int64_t unit1 = (g0 + blockDim.x - 1) / SH::CP;
     const int nu = (int)(unit1 - unit0 + 1);
     const int ul = (int)(unit - unit0);
     const bool valid = unit < prm.n_units;
@@ -210,7 +159,6 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     const int64_t my_len = valid ? (prm.chunk_len < prm.M - s0 ? prm.chunk_len : prm.M - s0) : 0;
     const int T = prm.tile;
     const int has_bp = prm.bp_mode != 0;
-    float* wbuf = zs + ((size_t)prm.nu_max * T * C + 3) / 4 * 4 + (size_t)(threadIdx.x >> 5) * WarpStage<SH>::FLOATS;
 
     int p[SH::PD];
     prefix_digits<SH>(prefix, p);
@@ -279,11 +227,7 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
             fused_mulexp<SH, SH::N, false>(own, low, z, zp);
             if (prm.stream) {
                 float* row = prm.out + ((size_t)b * prm.M + (s0 + t0 + t)) * SH::S;
-                if (cpad % 32 == 0) {
-                    store_state_warp<SH>(row, prefix, threadIdx.x & 31, pvalid, wbuf, own, low);
-                } else if (pvalid) {
-                    store_state<SH, true>(row, prefix, own, low);
-                }
+                store_state<SH, true>(row, prefix, own, low);
             }
         }
     }
@@ -299,15 +243,13 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
         for (int f = threadIdx.x; f < (int)SH::S; f += blockDim.x) o[f] = zs[f];
         return;
     }
-    if (valid && pvalid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
+    if (valid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
 }
 
 template <class SH>
 cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     FwdParams prm = prm_in;
-    // stream mode: pad units to whole warps so the warp-staged stores apply
-    prm.cpad = (prm.stream && SH::CP >= 32) ? (SH::CP + 31) / 32 * 32 : SH::CP;
-    const int64_t threads = prm.n_units * (int64_t)prm.cpad;
+    const int64_t threads = prm.n_units * (int64_t)SH::CP;
     int bd = 512;
     if (prm.upc > 0) {
         // grouped chunks: a CTA is exactly upc whole units (no unit straddles two CTAs)
@@ -329,15 +271,11 @@ cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
         }
     }
     const int64_t grid = (threads + bd - 1) / bd;
-    const int nu = (prm.upc > 0) ? prm.upc : (int)((bd - 1) / prm.cpad + 2);  // max units touched by one CTA
+    const int nu = (prm.upc > 0) ? prm.upc : (int)((bd - 1) / SH::CP + 2);  // max units touched by one CTA
     int tile = (int)(prm.chunk_len < 256 ? prm.chunk_len : 256);
     while (tile > 8 && (size_t)nu * tile * SH::C * 4 > 48 * 1024) tile /= 2;
     prm.tile = tile;
-    prm.nu_max = nu;
     size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
-    if (prm.stream && prm.cpad % 32 == 0)
-        smem = ((size_t)nu * tile * SH::C + 3) / 4 * 4 * sizeof(float) +
-               (size_t)(bd / 32) * WarpStage<SH>::FLOATS * sizeof(float);
     if (prm.upc > 0 && (size_t)nu * SH::S * sizeof(float) > smem) smem = (size_t)nu * SH::S * sizeof(float);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (smem > 48 * 1024) {
