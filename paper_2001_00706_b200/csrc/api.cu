@@ -9,8 +9,10 @@
 
 #include "../../include/sig.h"
 #define SIG_DEFINE_COMBINE_KERNELS
+#define SIG_DEFINE_LOGSIG_KERNELS
 #include "combine.cuh"
 #include "logsig.cuh"
+#include "logsig_owned.cuh"
 #include "lyndon.h"
 #include "sig_bwd.cuh"
 #include "sig_table.h"
@@ -310,8 +312,10 @@ LogsigTables device_view(const sig_logsig_plan_s* pl) {
     return tb;
 }
 
+constexpr size_t kMaxSmem = 227 * 1024 - 512;  // dynamic shared memory per CTA (static arrays need the rest)
+
 sig_status_t check_logsig_smem(const LDims& d, int64_t w, bool brackets) {
-    if (logsig_fwd_smem(d, (int)w, brackets) > 227 * 1024 || logsig_bwd_smem(d) > 227 * 1024)
+    if (logsig_fwd_smem(d, (int)w, brackets) > 227 * 1024 || logsig_bwd_smem(d, false) > kMaxSmem)
         return fail(SIG_ERR_UNSUPPORTED, "logsignature of C=%d depth=%d exceeds one CTA's shared memory", d.C, d.N);
     return SIG_OK;
 }
@@ -591,12 +595,27 @@ sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad
     p.gout = grad_out;
     p.gsig = gsig;
     p.glog_ws = glog;
-    const size_t smem = logsig_bwd_smem(p.d);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(logsig_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
+    const size_t smem_owned = logsig_bwd_owned_smem(p.d);
+    if (LogsigBwdLaunch fn = find_logsig_bwd_owned(plan->C, plan->N)) {
+        cudaError_t e = fn(p, (cudaStream_t)s);
+        if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");
+    } else if (smem_owned <= kMaxSmem) {
+        if (smem_owned > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(logsig_bwd_owned_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem_owned);
+            if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
+        }
+        logsig_bwd_owned_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem_owned, (cudaStream_t)s>>>(p);
+    } else {
+        p.gl_smem = logsig_bwd_smem(p.d, true) <= kMaxSmem;
+        const size_t smem = logsig_bwd_smem(p.d, p.gl_smem);
+        if (smem > 48 * 1024) {
+            cudaError_t e =
+                cudaFuncSetAttribute(logsig_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
+        }
+        logsig_bwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, (cudaStream_t)s>>>(p);
     }
-    logsig_bwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, (cudaStream_t)s>>>(p);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");

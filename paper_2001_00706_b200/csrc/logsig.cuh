@@ -96,10 +96,12 @@ struct LogsigParams {
     const float* gout;            // bwd: [rows, w|S]
     float* gsig;                  // bwd: [rows, S] output (accumulated in place)
     float* glog_ws;               // bwd scratch [rows, S]: dense dL/dlog (words / brackets)
+    int gl_smem;                  // bwd: dense dL/dlog staged in shared memory (else glog_ws)
 };
 
 constexpr int LOGSIG_THREADS = 1024;
 
+#ifdef SIG_DEFINE_LOGSIG_KERNELS  // non-template kernels: defined in api.cu only
 __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_fwd_kernel(const LogsigParams p) {
     const LDims& d = p.d;
     const int N = d.N, S = d.S;
@@ -172,6 +174,8 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_fwd_kernel(const Log
 // 32 lanes that split the inner index and combine with an xor-shuffle tree (fixed order:
 // deterministic).  gH is double-buffered so all levels of a pass are independent.  Each dL/dSig
 // coefficient has one owner and accumulates in place in the output row.
+#endif  // SIG_DEFINE_LOGSIG_KERNELS
+
 __device__ __forceinline__ int group_for(int work) {
     int G = 1;
     while (G < 32 && G * 16 < work) G <<= 1;
@@ -183,6 +187,7 @@ __device__ __forceinline__ float group_sum(float v, int G) {
     return v;
 }
 
+#ifdef SIG_DEFINE_LOGSIG_KERNELS  // non-template kernels: defined in api.cu only
 __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const LogsigParams p) {
     const LDims& d = p.d;
     const int N = d.N, S = d.S;
@@ -197,11 +202,38 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const Log
     float* Hall = lsf;                 // all H_n
     float* gHa = Hall + hb(0);         // [HS] dL/dH, double-buffered
     float* gHb = gHa + HS;             // [HS]
-    float* xs = gHb + HS;              // [S]
+    float* xs = gHb + HS;              // [off[N]] levels 1..N-1 of x (level N is never read)
     const float* src = p.sig + row * S;
-    for (int f = threadIdx.x; f < S; f += blockDim.x) xs[f] = src[f];
+    for (int f = threadIdx.x; f < d.off[N]; f += blockDim.x) xs[f] = src[f];
     if (threadIdx.x == 0) Hall[hb(N)] = 1.0f / (float)N;
+    // dense dL/dlog: shared memory when it fits (the passes below read it many times)
+    float* gw = p.gl_smem ? xs + d.off[N] : p.glog_ws + row * S;
+    if (p.mode == 0) {
+        if (p.gl_smem) {
+            const float* go = p.gout + row * S;
+            for (int f = threadIdx.x; f < S; f += blockDim.x) gw[f] = go[f];
+        } else {
+            gw = const_cast<float*>(p.gout + row * S);
+        }
+    } else {
+        for (int f = threadIdx.x; f < S; f += blockDim.x) gw[f] = 0.0f;
+    }
     __syncthreads();
+    if (p.mode != 0) {
+        const float* go = p.gout + row * p.tb.w;
+        for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
+            double v;
+            if (p.mode == 2) {
+                v = go[j];
+            } else {
+                v = 0.0;
+                for (int e = p.tb.minvT_rowptr[j]; e < p.tb.minvT_rowptr[j + 1]; ++e)
+                    v = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], v);
+            }
+            gw[(int)p.tb.lyn_idx[j]] = (float)v;
+        }
+    }
+    const float* gl = gw;
     for (int n = N - 1; n >= 1; --n) {
         const int top = N - n;
         float* Hn = Hall + hb(n);
@@ -226,103 +258,63 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const Log
         }
         __syncthreads();
     }
-    // dense dL/dlog
-    const float* gl;
-    if (p.mode == 0) {
-        gl = p.gout + row * S;
-    } else {
-        float* gw = p.glog_ws + row * S;
-        for (int f = threadIdx.x; f < S; f += blockDim.x) gw[f] = 0.0f;
-        __syncthreads();
-        const float* go = p.gout + row * p.tb.w;
-        for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
-            double v;
-            if (p.mode == 2) {
-                v = go[j];
-            } else {
-                v = 0.0;
-                for (int e = p.tb.minvT_rowptr[j]; e < p.tb.minvT_rowptr[j + 1]; ++e)
-                    v = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], v);
-            }
-            gw[(int)p.tb.lyn_idx[j]] = (float)v;
-        }
-        gl = gw;
-    }
     float* gx = p.gsig + row * S;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-
-    // Work lists: level l of a pass needs ns[l] warp slots of (32 / G[l]) outputs each.
-    __shared__ int s_G[17], s_ns[17];
-    auto plan_pass = [&](int lo, int hi, bool gx_kind, int top) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int l = lo; l <= hi; ++l) {
-                const int work = gx_kind ? d.hoff[top - l + 1] : d.off[top - l + 1];
-                const int G = group_for(work);
-                s_G[l] = G;
-                s_ns[l] = (d.pw[l] * G + 31) / 32;
-            }
-        }
-        __syncthreads();
-    };
+    // Both passes walk the output levels in turn; within a level, G lanes (a power of two <= 32,
+    // so groups never straddle a warp) share one output.  There is no barrier between levels, so
+    // threads done with a small level go straight on to the next one.
+    auto lg2 = [](int G) { return 31 - __clz(G); };
     // gx_i[u] (+)= sgn * sum_{m=0}^{top-i} sum_v src_{i+m}[u C^m + v] * Hm[v],  i = 1..top
     // src(level k, idx) = gl[off[k] + idx] (step A) or gHs[hoff[k] + idx]
     auto gx_pass = [&](int top, const float* gHs, const float* Hm, float sgn, bool init) {
-        plan_pass(1, top, true, top);
-        int total = 0;
-        for (int i = 1; i <= top; ++i) total += s_ns[i];
-        for (int slot = warp; slot < total; slot += nwarps) {
-            int i = 1, base = slot;
-            while (base >= s_ns[i]) {
-                base -= s_ns[i];
-                ++i;
-            }
-            const int G = s_G[i];
-            const int u = base * (32 / G) + lane / G, gq = lane % G;
-            float acc = 0.0f;
-            if (u < d.pw[i]) {
-                for (int m = 0; m <= top - i; ++m) {
-                    const int nv = d.pw[m];
-                    const float* srow = gHs ? gHs + d.hoff[i + m] + u * nv : gl + d.off[i + m] + u * nv;
-                    const float* hrow = Hm + d.hoff[m];
-                    for (int v = gq; v < nv; v += G) acc = fmaf(srow[v], hrow[v], acc);
+        for (int i = 1; i <= top; ++i) {
+            const int nout = d.pw[i];
+            const int G = group_for(d.hoff[top - i + 1]), sh = lg2(G);
+            const int items = ((nout << sh) + 31) & ~31;
+            for (int idx = threadIdx.x; idx < items; idx += blockDim.x) {
+                const int u = idx >> sh, gq = idx & (G - 1);
+                float acc = 0.0f;
+                if (u < nout) {
+                    const float* sb = gHs ? gHs + d.hoff[i] : gl + d.off[i];
+                    for (int m = 0; m <= top - i; ++m) {
+                        const int nv = d.pw[m];
+                        const float* srow = sb + u * nv;
+                        const float* hrow = Hm + d.hoff[m];
+#pragma unroll 4
+                        for (int v = gq; v < nv; v += G) acc = fmaf(srow[v], hrow[v], acc);
+                        sb += d.pw[i + m];  // next level's block
+                    }
                 }
-            }
-            acc = group_sum(acc, G);
-            if (gq == 0 && u < d.pw[i]) {
-                float* dst = &gx[d.off[i] + u];
-                *dst = init ? sgn * acc : fmaf(sgn, acc, *dst);
+                acc = group_sum(acc, G);
+                if (gq == 0 && u < nout) {
+                    float* dst = &gx[d.off[i] + u];
+                    *dst = init ? sgn * acc : fmaf(sgn, acc, *dst);
+                }
             }
         }
     };
     // gHo_m[v] = sgn * sum_{i=1}^{top-m} sum_u x_i[u] src_{i+m}[u C^m + v],  m = 1..top-1
     auto gh_pass = [&](int top, const float* gHs, float* gHo, float sgn) {
-        if (top < 2) return;
-        plan_pass(1, top - 1, false, top);
-        int total = 0;
-        for (int m = 1; m <= top - 1; ++m) total += s_ns[m];
-        for (int slot = warp; slot < total; slot += nwarps) {
-            int m = 1, base = slot;
-            while (base >= s_ns[m]) {
-                base -= s_ns[m];
-                ++m;
-            }
-            const int G = s_G[m];
-            const int v = base * (32 / G) + lane / G, gq = lane % G;
-            float acc = 0.0f;
-            if (v < d.pw[m]) {
-                const int stride = d.pw[m];
-                for (int i = 1; i <= top - m; ++i) {
-                    const int nu = d.pw[i];
-                    const float* xrow = xs + d.off[i];
-                    const float* srow = gHs ? gHs + d.hoff[i + m] + v : gl + d.off[i + m] + v;
-                    for (int u = gq; u < nu; u += G) acc = fmaf(xrow[u], srow[u * stride], acc);
+        for (int m = 1; m <= top - 1; ++m) {
+            const int nout = d.pw[m];
+            const int G = group_for(d.off[top - m + 1]), sh = lg2(G);
+            const int items = ((nout << sh) + 31) & ~31;
+            for (int idx = threadIdx.x; idx < items; idx += blockDim.x) {
+                const int v = idx >> sh, gq = idx & (G - 1);
+                float acc = 0.0f;
+                if (v < nout) {
+                    const int stride = nout;
+                    for (int i = 1; i <= top - m; ++i) {
+                        const int nu = d.pw[i];
+                        const float* xrow = xs + d.off[i];
+                        const float* srow = gHs ? gHs + d.hoff[i + m] + v : gl + d.off[i + m] + v;
+#pragma unroll 4
+                        for (int u = gq; u < nu; u += G) acc = fmaf(xrow[u], srow[u * stride], acc);
+                    }
                 }
+                acc = group_sum(acc, G);
+                if (gq == 0 && v < nout) gHo[d.hoff[m] + v] = sgn * acc;
             }
-            acc = group_sum(acc, G);
-            if (gq == 0 && v < d.pw[m]) gHo[d.hoff[m] + v] = sgn * acc;
         }
     };
     // step A: log = x H_1 (H_1 on levels 0..N-1)
@@ -342,14 +334,245 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_kernel(const Log
     }
 }
 
+#endif  // SIG_DEFINE_LOGSIG_KERNELS
+
+// ---------------------------------------------------------------------------------------------
+// K5, owned-prefix form (used whenever its shared-memory layout fits; logsig_bwd_kernel above is
+// the general fallback).  Each pass of the Horner VJP is a pair of contractions of a source
+// tensor s (dL/dlog, then dL/dH_n) on levels 1..top:
+//   GX: gx_i[u]  (+)= sgn * sum_{m=0}^{top-i} sum_v s_{i+m}[u v] H_m[v]          (trailing contraction)
+//   GH: gH_m[v]   = sgn * sum_{i=1}^{top-m} sum_u x_i[u] s_{i+m}[u v]            (leading contraction)
+// GX is split by word PREFIX: thread p (a word of length P' = min(P, top)) computes every output
+// gx_i[u] with u[:P'] = p outright (i >= P'), and for i < P' one partial over the words it owns,
+// which an aligned block of C^(P'-i) threads then sums.  GH is split the same way by word SUFFIX.
+// Every thread does about the same number of FMAs; source reads are thread-strided blocks, so the
+// shared arrays carry one pad float per 32 (lpad) to keep them conflict-free.  All sums have a
+// fixed order.
+__host__ __device__ constexpr inline int lpad(int e) { return e + (e >> 5); }
+
+struct OwnedLayout {
+    int P;                                       // ownership prefix length (C^P <= 1024)
+    int o_gha, o_ghb, o_xs, o_gl, o_scr, total;  // float offsets into shared memory (H_n at 0)
+};
+
+__host__ __device__ inline int hall_size(const LDims& d) {
+    int hall = 0;
+    for (int n = 1; n <= d.N; ++n) hall += d.hoff[d.N - n + 1];
+    return hall;
+}
+
+__host__ __device__ inline OwnedLayout owned_layout(const LDims& d) {
+    OwnedLayout L;
+    int P = 1;
+    while (P < d.N && d.pw[P + 1] <= LOGSIG_THREADS) ++P;
+    L.P = P;
+    const int hs = d.hoff[d.N];
+    const int scr = (P > 1 ? P - 1 : 1) * d.pw[P];
+    L.o_gha = lpad(hall_size(d)) + 1;
+    L.o_ghb = L.o_gha + lpad(hs) + 1;
+    L.o_xs = L.o_ghb + lpad(hs) + 1;
+    L.o_gl = L.o_xs + d.off[d.N];
+    L.o_scr = L.o_gl + lpad(d.S) + 1;
+    L.total = L.o_scr + lpad(scr) + 1;
+    return L;
+}
+
+// sum aligned blocks of a partial row: level l (1..Lp-1) has C^l outputs, each the sum of the
+// C^(Lp-l) consecutive entries of row l-1 (rows of np entries); G lanes per output
+template <class Emit>
+__device__ __forceinline__ void owned_block_reduce(const LDims& d, const float* scr, int Lp, int np, Emit&& emit) {
+    for (int l = 1; l < Lp; ++l) {
+        const int nout = d.pw[l], bs = d.pw[Lp - l];
+        int G = 1;
+        while (G < 32 && 2 * G <= bs) G <<= 1;
+        const int sh = 31 - __clz(G);
+        const int items = ((nout << sh) + 31) & ~31;
+        for (int idx = threadIdx.x; idx < items; idx += blockDim.x) {
+            const int o = idx >> sh, g = idx & (G - 1);
+            float sum = 0.0f;
+            if (o < nout) {
+                const int base = (l - 1) * np + o * bs;
+                for (int e = g; e < bs; e += G) sum += scr[lpad(base + e)];
+            }
+            for (int q = G >> 1; q >= 1; q >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, q);
+            if (g == 0 && o < nout) emit(l, o, sum);
+        }
+    }
+}
+
+// one pass: src levels k at src[lpad(soff[k] + idx)], H_m at Hall[lpad(hbase + hoff[m] + idx)]
+__device__ __forceinline__ void owned_pass(const LDims& d, int P, int top, const float* src, const int* soff,
+                                           const float* Hall, int hbase, const float* xs, float* scr, float* gx,
+                                           float* gHo, float sgn, bool init) {
+    const int tid = threadIdx.x, nth = blockDim.x;
+    auto Sv = [&](int e) { return src[lpad(e)]; };
+    auto Hv = [&](int e) { return Hall[lpad(hbase + e)]; };
+    // ---- GX, by prefix
+    const int Pg = P < top ? P : top;
+    const int np = d.pw[Pg];
+    for (int pf = tid; pf < np; pf += nth) {
+        for (int i = Pg; i <= top; ++i) {  // owned outputs u = pf u'
+            const int nu = d.pw[i - Pg];
+            for (int up = 0; up < nu; ++up) {
+                const int u = pf * nu + up;
+                float acc = 0.0f;
+                for (int m = 0; m <= top - i; ++m) {
+                    const int nv = d.pw[m];
+                    const int rb = soff[i + m] + u * nv, hb0 = d.hoff[m];
+                    for (int v = 0; v < nv; ++v) acc = fmaf(Sv(rb + v), Hv(hb0 + v), acc);
+                }
+                float* dst = gx + d.off[i] + u;
+                *dst = init ? sgn * acc : fmaf(sgn, acc, *dst);
+            }
+        }
+        for (int i = 1; i < Pg; ++i) {  // partial of gx_i[p[:i]] over the words this thread owns
+            const int ps = pf % d.pw[Pg - i];  // p[i:]
+            float acc = 0.0f;
+            for (int k = Pg; k <= top; ++k) {  // words p v'
+                const int nv = d.pw[k - Pg];
+                const int sb = soff[k] + pf * nv, hb0 = d.hoff[k - i] + ps * nv;
+                for (int v = 0; v < nv; ++v) acc = fmaf(Sv(sb + v), Hv(hb0 + v), acc);
+            }
+            for (int k = i; k < Pg; ++k) {  // short words w (|w| = k < P'), owned by p = w 0..0
+                const int q = d.pw[Pg - k];
+                if (pf % q == 0) {
+                    const int w = pf / q;
+                    acc = fmaf(Sv(soff[k] + w), Hv(d.hoff[k - i] + w % d.pw[k - i]), acc);
+                }
+            }
+            scr[lpad((i - 1) * np + pf)] = acc;
+        }
+    }
+    __syncthreads();
+    owned_block_reduce(d, scr, Pg, np, [&](int i, int u, float sum) {
+        float* dst = gx + d.off[i] + u;
+        *dst = init ? sgn * sum : fmaf(sgn, sum, *dst);
+    });
+    if (!gHo || top < 2) return;
+    __syncthreads();  // scratch reuse
+    // ---- GH, by suffix
+    const int Ph = P < top - 1 ? P : top - 1;
+    const int ns = d.pw[Ph];
+    for (int sf = tid; sf < ns; sf += nth) {
+        for (int m = Ph; m <= top - 1; ++m) {  // owned outputs v = v'' s
+            const int nvv = d.pw[m - Ph], stride = d.pw[m];
+            for (int vv = 0; vv < nvv; ++vv) {
+                const int v = vv * ns + sf;
+                float acc = 0.0f;
+                for (int i = 1; i <= top - m; ++i) {
+                    const int nu = d.pw[i], xb = d.off[i], sb = soff[i + m] + v;
+                    for (int u = 0; u < nu; ++u) acc = fmaf(xs[xb + u], Sv(sb + u * stride), acc);
+                }
+                gHo[lpad(d.hoff[m] + v)] = sgn * acc;
+            }
+        }
+        for (int m = 1; m < Ph; ++m) {  // partial of gH_m[s[Ph-m:]] over the words this thread owns
+            const int cm = d.pw[m], sq = sf / cm, cq = d.pw[Ph - m];
+            float acc = 0.0f;
+            for (int k = Ph; k <= top; ++k) {  // words y s, split u = (y s)[:k-m]
+                const int ny = d.pw[k - Ph], xb = d.off[k - m] + sq, sb = soff[k] + sf;
+                for (int y = 0; y < ny; ++y) acc = fmaf(xs[xb + y * cq], Sv(sb + y * ns), acc);
+            }
+            for (int k = m + 1; k < Ph; ++k)  // short words w = s (|w| = k), owned by s = 0..0 w
+                if (sf < d.pw[k]) acc = fmaf(xs[d.off[k - m] + sq], Sv(soff[k] + sf), acc);
+            scr[lpad((m - 1) * ns + (sf % cm) * cq + sq)] = acc;  // grouped by output
+        }
+    }
+    __syncthreads();
+    owned_block_reduce(d, scr, Ph, ns, [&](int m, int v, float sum) { gHo[lpad(d.hoff[m] + v)] = sgn * sum; });
+}
+
+#ifdef SIG_DEFINE_LOGSIG_KERNELS  // non-template kernels: defined in api.cu only
+__global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_owned_kernel(const LogsigParams p) {
+    const LDims& d = p.d;
+    const int N = d.N, S = d.S;
+    const int64_t row = blockIdx.x;
+    const OwnedLayout L = owned_layout(d);
+    extern __shared__ __align__(16) float lsf[];
+    auto hb = [&](int n) -> int {  // offset of H_n (levels 0..N-n) in Hall; H_N first
+        int s = 0;
+        for (int q = N; q > n; --q) s += d.hoff[N - q + 1];
+        return s;
+    };
+    float* Hall = lsf;
+    float* gHa = lsf + L.o_gha;
+    float* gHb = lsf + L.o_ghb;
+    float* xs = lsf + L.o_xs;  // levels 1..N-1 of x
+    float* gl = lsf + L.o_gl;  // dense dL/dlog, padded
+    float* scr = lsf + L.o_scr;
+    const float* sg = p.sig + row * S;
+    for (int f = threadIdx.x; f < d.off[N]; f += blockDim.x) xs[f] = sg[f];
+    if (threadIdx.x == 0) Hall[lpad(hb(N))] = 1.0f / (float)N;
+    if (p.mode == 0) {
+        const float* go = p.gout + row * S;
+        for (int f = threadIdx.x; f < S; f += blockDim.x) gl[lpad(f)] = go[f];
+    } else {
+        for (int f = threadIdx.x; f < S; f += blockDim.x) gl[lpad(f)] = 0.0f;
+        __syncthreads();
+        const float* go = p.gout + row * p.tb.w;
+        for (int j = threadIdx.x; j < p.tb.w; j += blockDim.x) {
+            double v;
+            if (p.mode == 2) {
+                v = go[j];
+            } else {
+                v = 0.0;
+                for (int e = p.tb.minvT_rowptr[j]; e < p.tb.minvT_rowptr[j + 1]; ++e)
+                    v = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], v);
+            }
+            gl[lpad((int)p.tb.lyn_idx[j])] = (float)v;
+        }
+    }
+    __syncthreads();
+    // recompute H_{N-1} .. H_1 (float: the VJP has no cancellation problem)
+    for (int n = N - 1; n >= 1; --n) {
+        const int top = N - n, bn = hb(n), bc = hb(n + 1);
+        for (int e = threadIdx.x; e < d.hoff[top + 1]; e += blockDim.x) {
+            float val = 1.0f / (float)n;
+            if (e > 0) {
+                const int m = hlvl_of(d, e);
+                float acc = 0.0f;
+                int u = e - d.hoff[m], v = 0, q = 1;
+                for (int i = m; i >= 1; --i) {
+                    acc = fmaf(xs[d.off[i] + u], Hall[lpad(bc + d.hoff[m - i] + v)], acc);
+                    const int u2 = divC(d, u);
+                    v += (u - u2 * d.C) * q;
+                    q *= d.C;
+                    u = u2;
+                }
+                val = -acc;
+            }
+            Hall[lpad(bn + e)] = val;
+        }
+        __syncthreads();
+    }
+    float* gx = p.gsig + row * S;
+    // step A: log = x H_1
+    owned_pass(d, L.P, N, gl, d.off, Hall, hb(1), xs, scr, gx, N >= 2 ? gHa : nullptr, 1.0f, true);
+    __syncthreads();
+    float* gc = gHa;
+    float* gn = gHb;
+    for (int n = 1; n <= N - 1; ++n) {  // H_n = 1/n - x H_{n+1}; gc = dL/dH_n on levels 1..N-n
+        owned_pass(d, L.P, N - n, gc, d.hoff, Hall, hb(n + 1), xs, scr, gx, n <= N - 2 ? gn : nullptr, -1.0f,
+                   false);
+        __syncthreads();
+        float* t = gc;
+        gc = gn;
+        gn = t;
+    }
+}
+
+#endif  // SIG_DEFINE_LOGSIG_KERNELS
+
+inline size_t logsig_bwd_owned_smem(const LDims& d) { return (size_t)owned_layout(d).total * sizeof(float); }
+
 inline size_t logsig_fwd_smem(const LDims& d, int w, bool brackets) {
     return (size_t)(2 * d.hoff[d.N]) * sizeof(double) + (size_t)(d.S + (brackets ? w : 0)) * sizeof(float);
 }
 
-inline size_t logsig_bwd_smem(const LDims& d) {
+inline size_t logsig_bwd_smem(const LDims& d, bool gl_smem) {
     int hall = 0;
     for (int n = 1; n <= d.N; ++n) hall += d.hoff[d.N - n + 1];
-    return (size_t)(hall + 2 * d.hoff[d.N] + d.S) * sizeof(float);
+    return (size_t)(hall + 2 * d.hoff[d.N] + d.off[d.N] + (gl_smem ? d.S : 0)) * sizeof(float);
 }
 
 }  // namespace sigb200

@@ -1,0 +1,35 @@
+// logsig_owned.cu -- instances of the compile-time K5 (logsig_owned.cuh) and their lookup.
+#include <utility>
+#include "logsig_owned.cuh"
+
+namespace sigb200 {
+namespace {
+
+constexpr size_t kOwnedMaxSmem = 227 * 1024 - 512;
+
+template <int C, int N>
+constexpr LogsigBwdLaunch entry() {
+    if constexpr ((size_t)LT<C, N>::TOTAL * sizeof(float) <= kOwnedMaxSmem) return &launch_logsig_bwd_owned_t<C, N>;
+    else return nullptr;
+}
+
+template <int C, int... Ns>
+LogsigBwdLaunch pick(int N, std::integer_sequence<int, Ns...>) {
+    LogsigBwdLaunch r = nullptr;
+    ((N == Ns + 1 ? (r = entry<C, Ns + 1>(), 0) : 0), ...);
+    return r;
+}
+
+}  // namespace
+
+LogsigBwdLaunch find_logsig_bwd_owned(int C, int N) {
+    switch (C) {
+        case 1: return pick<1>(N, std::make_integer_sequence<int, 12>{});
+        case 2: return pick<2>(N, std::make_integer_sequence<int, 12>{});
+        case 4: return pick<4>(N, std::make_integer_sequence<int, 7>{});
+        case 8: return pick<8>(N, std::make_integer_sequence<int, 5>{});
+        default: return nullptr;
+    }
+}
+
+}  // namespace sigb200

@@ -27,7 +27,9 @@ def _blocks(C, N, mode):
     return [(lv.index(k), len(lv) - lv[::-1].index(k)) for k in range(1, N + 1) if k in lv]
 
 
-LOG_CASES = [(4, 7, 4, 64), (3, 4, 5, 30), (2, 5, 6, 20), (8, 3, 3, 40), (4, 4, 8, 128)]
+# (3,7), (5,5), (6,4) have ownership prefix P < N in the owned-prefix backward (non power-of-two C)
+LOG_CASES = [(4, 7, 4, 64), (3, 4, 5, 30), (2, 5, 6, 20), (8, 3, 3, 40), (4, 4, 8, 128), (3, 7, 3, 20), (5, 5, 3, 16),
+             (6, 4, 3, 16)]
 
 
 @pytest.mark.parametrize("mode", ["words", "brackets", "expand"])
@@ -43,8 +45,13 @@ def test_logsignature_forward(mode, C, N, B, L):
 
 
 @pytest.mark.parametrize("mode", ["words", "brackets", "expand"])
-@pytest.mark.parametrize("C,N,B,L", [(4, 7, 3, 48), (3, 4, 4, 20), (2, 5, 3, 15), (8, 3, 2, 30)])
+@pytest.mark.parametrize("C,N,B,L", [(4, 7, 3, 48), (3, 4, 4, 20), (2, 5, 3, 15), (8, 3, 2, 30), (3, 7, 2, 12),
+                                     (5, 5, 2, 10), (8, 5, 2, 6)])
 def test_logsignature_backward(mode, C, N, B, L):
+    """K5 in its three forms: compiled per (C, N) for power-of-two C (4,7), (2,5), (8,3); the runtime
+    owned-prefix kernel (3,4), (3,7), (5,5); the general fallback (8,5) (owned layout too large)."""
+    if mode == "brackets" and (C, N) == (8, 5):
+        pytest.skip("brackets at C=8, N=5 exceed one CTA's shared memory in K4 (UNSUPPORTED)")
     x = brownian_paths(B, L, C, seed=3 * C + N)
     w = sb.sig_logsignature_channels(C, N, mode)
     g = normal((B, w), seed=104)
@@ -126,3 +133,27 @@ def test_multi_combine_chen(n):
     sigs = np.stack([oracle.signature(x[:, 4 * j:4 * j + 5], N) for j in range(pieces)]).astype(np.float32)
     got = sb.multi_signature_combine(_cuda(sigs), C, N).cpu().numpy()
     assert level_rel_err(got, oracle.signature(x, N), C, N) < FWD_TOL
+
+
+_POW2_INSTANCES = [(C, N) for C in (1, 2, 4, 8) for N in range(1, 13) if sum(C ** k for k in range(1, N + 1)) <= 6000]
+
+
+@pytest.mark.parametrize("C,N", _POW2_INSTANCES)
+def test_logsignature_backward_every_compiled_instance(C, N):
+    """Every compiled (C, N) instance of the owned-prefix K5 (expand and words), small paths."""
+    x = brownian_paths(2, 6, C, seed=C * 31 + N)
+    for mode in ("expand", "words"):
+        w = sb.sig_logsignature_channels(C, N, mode)
+        g = normal((2, w), seed=7)
+        xt = _cuda(x).requires_grad_(True)
+        sb.logsignature(xt, N, mode).backward(_cuda(g))
+        ref, _ = oracle.logsignature_vjp(g, x, N, mode=mode)
+        got = xt.grad.cpu().numpy()
+        if C == 1:
+            # one channel: log = (increment, 0, ..., 0), so the path gradient is +-g_1 at the end
+            # points, reached through cancelling O(|g|) terms; scale the error by |g| (not the
+            # possibly tiny |g_1| of one path)
+            err = np.abs(got - ref).max() / max(np.abs(ref).max(), np.abs(g).max())
+        else:
+            err = path_rel_err(got, ref)
+        assert err < BWD_TOL, (C, N, mode, err)
