@@ -16,6 +16,9 @@ Every function follows the paper's definitions, cited as P:Lnnn = line of PAPER.
   logsignature        log, then words = psi, brackets = solve phi(x) = log,
                       expand = log itself
   combine             [x]; multi_combine = left fold
+  signature_ex        inverse (Sig(x)^-1 = Sig(reversed x), per prefix when streaming)
+                      and initial (initial [x] Sig; with inverse Sig^-1 [x] initial,
+                      reading R18); signature_vjp_ex = plain reverse mode through it
 """
 from __future__ import annotations
 
@@ -214,6 +217,80 @@ def signature_vjp(grad_out, path, depth: int, stream: bool = False, basepoint=No
         return gx, None
     gbp = gx[:, 0, :].copy()
     return np.ascontiguousarray(gx[:, 1:, :]), (None if basepoint is True or isinstance(basepoint, str) else gbp)
+
+
+def signature_ex(path, depth: int, stream: bool = False, basepoint=None, inverse: bool = False,
+                 initial=None, threads: int = 1) -> np.ndarray:
+    """signature with the inverse / initial options (reading R18).
+
+    inverse: Sig(x)^{-1} = Sig(x reversed), computed by definition on the reversed
+    (augmented) stream -- for stream=True on every reversed prefix (x_{t+1}, ..., x_0).
+    initial [B, S]: the result is initial [x] Sig (the update case); with inverse the
+    result is Sig^{-1} [x] initial (initial being the inverse of the earlier signature, since
+    (A [x] B)^{-1} = B^{-1} [x] A^{-1})."""
+    x = _with_basepoint(path, basepoint)
+    B, L, C = x.shape
+    if not inverse:
+        base = signature(x, depth, stream=stream, threads=threads)
+    elif not stream:
+        base = signature(np.ascontiguousarray(x[:, ::-1]), depth, threads=threads)
+    else:
+        base = np.stack([signature(np.ascontiguousarray(x[:, t + 1::-1]), depth, threads=threads)
+                         for t in range(L - 1)], axis=1)
+    if initial is None:
+        return base
+    ini = _f64(initial)
+    out = np.empty_like(base)
+    for b in range(B):
+        rows = base[b] if stream else base[b][None]
+        res = [mul(r, ini[b], C, depth) if inverse else mul(ini[b], r, C, depth) for r in rows]
+        out[b] = np.stack(res) if stream else res[0]
+    return out
+
+
+def signature_vjp_ex(grad_out, path, depth: int, stream: bool = False, basepoint=None, inverse: bool = False,
+                     initial=None, threads: int = 1):
+    """Reverse mode through signature_ex: (grad_path, grad_basepoint or None, grad_initial or None)."""
+    x = _with_basepoint(path, basepoint)
+    B, L, C = x.shape
+    g = _f64(grad_out)
+    ginit = None
+    if initial is not None:
+        # through the [x] with initial: gradient w.r.t. the plain (inverse) signature and initial
+        ini = _f64(initial)
+        base = signature_ex(path, depth, stream=stream, basepoint=basepoint, inverse=inverse, threads=threads)
+        gbase = np.empty_like(base)
+        ginit = np.zeros_like(ini)
+        for b in range(B):
+            rows = range(L - 1) if stream else [None]
+            for t in rows:
+                r = base[b, t] if stream else base[b]
+                gr = g[b, t] if stream else g[b]
+                if inverse:
+                    ga, gi = mul_vjp(gr, r, ini[b], C, depth)
+                else:
+                    gi, ga = mul_vjp(gr, ini[b], r, C, depth)
+                ginit[b] += gi
+                if stream:
+                    gbase[b, t] = ga
+                else:
+                    gbase[b] = ga
+        g = gbase
+    if not inverse:
+        gx, _ = signature_vjp(g, x, depth, stream=stream, threads=threads)
+    elif not stream:
+        gr, _ = signature_vjp(g, np.ascontiguousarray(x[:, ::-1]), depth, threads=threads)
+        gx = gr[:, ::-1]
+    else:
+        gx = np.zeros((B, L, C))
+        for t in range(L - 1):
+            gr, _ = signature_vjp(g[:, t], np.ascontiguousarray(x[:, t + 1::-1]), depth, threads=threads)
+            gx[:, :t + 2] += gr[:, ::-1]
+    gx = np.ascontiguousarray(gx)
+    if basepoint is None or basepoint is False:
+        return gx, None, ginit
+    gbp = None if (basepoint is True or isinstance(basepoint, str)) else gx[:, 0, :].copy()
+    return np.ascontiguousarray(gx[:, 1:, :]), gbp, ginit
 
 
 def combine(a, b, C: int, N: int) -> np.ndarray:
