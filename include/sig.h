@@ -110,6 +110,41 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
                                     const float* basepoint, float* grad_path, float* grad_basepoint,
                                     sig_cuda_stream_t s);
 
+/* ---------------------------------------------------------------- signature options */
+
+/* The `inverse` and `initial` options (reading R18).
+ *   inverse = 0: out = I [x] Sig(x)              (I = initial, or the identity when NULL)
+ *   inverse = 1: out = Sig(x)^{-1} [x] I, where Sig(x)^{-1} = Sig(x reversed); with
+ *                stream = 1, row t is the inverse of the prefix signature, [x] I.
+ * `initial` [B, S] (device) is the signature of the data seen before (inverse = 0), or its inverse
+ * (inverse = 1) -- the update case of P:L252-258: feed the new points with basepoint = the last
+ * old point.  Any [B, S] tensor is accepted; it is not checked to be group-like.
+ * Everything else as sig_signature.  Implementation: inverse scans the negated path from
+ * alpha(I) and reverses the words of the output (alpha = word reversal); it needs
+ * sig_signature_ex_workspace_size(...) bytes of workspace (B * S floats more than the plain
+ * scan when initial is given). */
+size_t sig_signature_ex_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                                       sig_basepoint_t bp, int32_t inverse, int32_t has_initial);
+sig_status_t sig_signature_ex(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                              sig_basepoint_t bp, const float* basepoint, int32_t inverse, const float* initial,
+                              float* out, void* ws, size_t ws_bytes, sig_cuda_stream_t s);
+
+/* Backward of sig_signature_ex (reversible, as sig_signature_backward).
+ *   grad_initial [B, S] or NULL: overwritten with the gradient w.r.t. `initial` (the scan's start
+ *                state) when given
+ *   ws           sig_signature_backward_ex_workspace_size(...) bytes: 0 for inverse = 0; for
+ *                inverse = 1 the alpha images of grad_out, the final state, initial and
+ *                grad_initial ((rows + up to 3 B) * S floats, rows = B or B*M)
+ * Errors as sig_signature_backward; WORKSPACE when ws is too small. */
+size_t sig_signature_backward_ex_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                                                sig_basepoint_t bp, int32_t inverse, int32_t has_initial,
+                                                int32_t want_grad_initial);
+sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path, const float* out_saved, int64_t B,
+                                       int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
+                                       const float* basepoint, int32_t inverse, const float* initial,
+                                       float* grad_path, float* grad_basepoint, float* grad_initial, void* ws,
+                                       size_t ws_bytes, sig_cuda_stream_t s);
+
 /* ---------------------------------------------------------------- combine (K3) */
 
 /* out[b] = a[b] [x] b[b] for b < B; all [B, S]. out must not alias a or b. */

@@ -68,6 +68,15 @@ def lib():
                                                  _vp, _c_sz, _vp]),
                 ("sig_signature_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32,
                                                           ctypes.c_int, _vp, _vp, _vp, _vp]),
+                ("sig_signature_ex_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32, ctypes.c_int,
+                                                            _c_i32, _c_i32]),
+                ("sig_signature_ex", ctypes.c_int, [_vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32, ctypes.c_int, _vp,
+                                                    _c_i32, _vp, _vp, _vp, _c_sz, _vp]),
+                ("sig_signature_backward_ex_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32,
+                                                                     ctypes.c_int, _c_i32, _c_i32, _c_i32]),
+                ("sig_signature_backward_ex", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32,
+                                                             ctypes.c_int, _vp, _c_i32, _vp, _vp, _vp, _vp, _vp,
+                                                             _c_sz, _vp]),
                 ("sig_signature_combine", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _vp]),
                 ("sig_signature_combine_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _vp,
                                                                   _vp]),
@@ -141,7 +150,9 @@ def sig_is_supported(C: int, depth: int, backward: bool = False) -> bool:
     return bool(lib().sig_is_supported(C, depth, int(backward)))
 
 
-def sig_signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None) -> torch.Tensor:
+def sig_signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None, inverse: bool = False,
+                  initial=None) -> torch.Tensor:
+    """sig_signature / sig_signature_ex: inverse and initial as in include/sig.h (reading R18)."""
     path = _dev_f32(path, "path")
     B, L, C = path.shape
     bpm, bp = _bp(basepoint, path)
@@ -151,10 +162,17 @@ def sig_signature(path: torch.Tensor, depth: int, stream: bool = False, basepoin
         raise SigError(f"bad C={C} depth={depth}")
     M = L - 1 + (bpm != BP_NONE)
     out = torch.empty((B, M, S) if stream else (B, S), device=path.device, dtype=torch.float32)
-    wsb = Lib.sig_signature_workspace_size(B, L, C, depth, int(stream), bpm)
+    if not inverse and initial is None:
+        wsb = Lib.sig_signature_workspace_size(B, L, C, depth, int(stream), bpm)
+        ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+        _check(Lib.sig_signature(_ptr(path), B, L, C, depth, int(stream), bpm, _ptr(bp), _ptr(out), _ptr(ws), wsb,
+                                 _stream(path.device)), "sig_signature")
+        return out
+    ini = None if initial is None else _dev_f32(initial, "initial")
+    wsb = Lib.sig_signature_ex_workspace_size(B, L, C, depth, int(stream), bpm, int(inverse), int(ini is not None))
     ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
-    _check(Lib.sig_signature(_ptr(path), B, L, C, depth, int(stream), bpm, _ptr(bp), _ptr(out), _ptr(ws), wsb,
-                             _stream(path.device)), "sig_signature")
+    _check(Lib.sig_signature_ex(_ptr(path), B, L, C, depth, int(stream), bpm, _ptr(bp), int(inverse), _ptr(ini),
+                                _ptr(out), _ptr(ws), wsb, _stream(path.device)), "sig_signature_ex")
     return out
 
 
@@ -170,6 +188,29 @@ def sig_signature_backward(grad_out, path, out_saved, depth: int, stream: bool =
                                         _ptr(bp), _ptr(gp), _ptr(gbp), _stream(path.device)),
            "sig_signature_backward")
     return gp, gbp
+
+
+def sig_signature_backward_ex(grad_out, path, out_saved, depth: int, stream: bool = False, basepoint=None,
+                              inverse: bool = False, initial=None, want_grad_initial: bool = True):
+    """-> (grad_path, grad_basepoint or None, grad_initial or None)."""
+    path = _dev_f32(path, "path")
+    grad_out = _dev_f32(grad_out, "grad_out")
+    out_saved = _dev_f32(out_saved, "out_saved")
+    B, L, C = path.shape
+    bpm, bp = _bp(basepoint, path)
+    ini = None if initial is None else _dev_f32(initial, "initial")
+    Lib = lib()
+    S = Lib.sig_signature_channels(C, depth)
+    gp = torch.empty_like(path)
+    gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
+    gi = torch.empty((B, S), device=path.device, dtype=torch.float32) if want_grad_initial else None
+    wsb = Lib.sig_signature_backward_ex_workspace_size(B, L, C, depth, int(stream), bpm, int(inverse),
+                                                       int(ini is not None), int(gi is not None))
+    ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_signature_backward_ex(_ptr(grad_out), _ptr(path), _ptr(out_saved), B, L, C, depth, int(stream),
+                                         bpm, _ptr(bp), int(inverse), _ptr(ini), _ptr(gp), _ptr(gbp), _ptr(gi),
+                                         _ptr(ws), wsb, _stream(path.device)), "sig_signature_backward_ex")
+    return gp, gbp, gi
 
 
 def sig_signature_combine(a, b, C: int, depth: int):
@@ -271,19 +312,24 @@ def sig_logsignature_backward(grad_out, path, sig_saved, depth: int, mode: str =
 # ------------------------------------------------------------------------------------------------
 class _Signature(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, path, depth, stream, basepoint_flag, bp_tensor):
+    def forward(ctx, path, depth, stream, basepoint_flag, bp_tensor, inverse, initial):
         bp = bp_tensor if basepoint_flag == BP_GIVEN else (basepoint_flag == BP_ZERO)
-        out = sig_signature(path, depth, stream, bp)
-        ctx.save_for_backward(path, out, bp_tensor if basepoint_flag == BP_GIVEN else None)
-        ctx.depth, ctx.stream, ctx.bpf = depth, stream, basepoint_flag
+        out = sig_signature(path, depth, stream, bp, inverse=inverse, initial=initial)
+        ctx.save_for_backward(path, out, bp_tensor if basepoint_flag == BP_GIVEN else None, initial)
+        ctx.depth, ctx.stream, ctx.bpf, ctx.inverse = depth, stream, basepoint_flag, inverse
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
-        path, out, bpt = ctx.saved_tensors
+        path, out, bpt, initial = ctx.saved_tensors
         bp = bpt if ctx.bpf == BP_GIVEN else (ctx.bpf == BP_ZERO)
-        gp, gbp = sig_signature_backward(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp)
-        return gp, None, None, None, gbp
+        if not ctx.inverse and initial is None:
+            gp, gbp = sig_signature_backward(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp)
+            return gp, None, None, None, gbp, None, None
+        gp, gbp, gi = sig_signature_backward_ex(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp,
+                                                inverse=ctx.inverse, initial=initial,
+                                                want_grad_initial=initial is not None and ctx.needs_input_grad[6])
+        return gp, None, None, None, gbp, None, gi
 
 
 def _bp_args(basepoint):
@@ -294,11 +340,14 @@ def _bp_args(basepoint):
     return BP_GIVEN, basepoint
 
 
-def signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None) -> torch.Tensor:
+def signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None, inverse: bool = False,
+              initial=None) -> torch.Tensor:
     """Sig^depth of each stream in path [B, L, C] -> [B, S] (or [B, M, S] with stream=True).
-    Differentiable; the backward is the reversible handwritten kernel."""
+    inverse: Sig(x)^{-1} = Sig(x reversed); initial [B, S]: the update case
+     -- initial [x] Sig, or Sig^{-1} [x] initial with inverse (reading R18).
+    Differentiable in path, basepoint and initial; the backward is the reversible kernel."""
     f, t = _bp_args(basepoint)
-    return _Signature.apply(path, depth, stream, f, t)
+    return _Signature.apply(path, depth, stream, f, t, bool(inverse), initial)
 
 
 class _LogSignature(torch.autograd.Function):

@@ -230,9 +230,20 @@ cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_
     return cudaSuccess;
 }
 
+cudaError_t launch_word_reverse(const TensorDims& d, const float* in, int64_t si, float* out, int64_t so,
+                                int64_t rows, cudaStream_t s) {
+    const int64_t n = rows * d.S;
+    if (n == 0) return cudaSuccess;
+    word_reverse_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, in, si, out, so, rows);
+    count_launch();
+    return cudaGetLastError();
+}
+
+inline size_t align256(size_t n) { return (n + 255) / 256 * 256; }
+
 sig_status_t run_signature(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
                            sig_basepoint_t bp, const float* basepoint, float* out, void* ws, size_t ws_bytes,
-                           cudaStream_t s) {
+                           cudaStream_t s, float zsign = 1.0f, const float* initial = nullptr) {
     FwdPlan pl;
     sig_status_t st = make_fwd_plan(B, L, C, depth, stream, bp, pl);
     if (st != SIG_OK) return st;
@@ -255,6 +266,8 @@ sig_status_t run_signature(const float* path, int64_t B, int64_t L, int64_t C, i
     prm.n_units = B * pl.n_chunks;
     prm.upc = pl.upc;
     prm.dims = d;
+    prm.zsign = zsign;
+    prm.initial = initial;
     float* units = (pl.n_chunks > 1 && pl.n_parts > 1) ? static_cast<float*>(ws) : out;
     prm.out = units;
     cudaError_t e = pl.launch(prm, s);
@@ -370,10 +383,62 @@ sig_status_t sig_signature(const float* path, int64_t B, int64_t L, int64_t C, i
     return run_signature(path, B, L, C, depth, stream, bp, basepoint, out, ws, ws_bytes, (cudaStream_t)s);
 }
 
-sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
-                                    int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
-                                    const float* basepoint, float* grad_path, float* grad_basepoint,
-                                    sig_cuda_stream_t s) {
+size_t sig_signature_ex_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                                       sig_basepoint_t bp, int32_t inverse, int32_t has_initial) {
+    FwdPlan pl;
+    if (make_fwd_plan(B, L, C, depth, stream, bp, pl) != SIG_OK) return 0;
+    if (!inverse || !has_initial) return pl.ws_bytes;
+    return align256(pl.ws_bytes) + (size_t)B * (size_t)sig_channels_checked(C, depth) * sizeof(float);
+}
+
+sig_status_t sig_signature_ex(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                              sig_basepoint_t bp, const float* basepoint, int32_t inverse, const float* initial,
+                              float* out, void* ws, size_t ws_bytes, sig_cuda_stream_t s) {
+    if (!inverse)
+        return run_signature(path, B, L, C, depth, stream, bp, basepoint, out, ws, ws_bytes, (cudaStream_t)s, 1.0f,
+                             initial);
+    // inverse (reading R18): scan the negated path from alpha(initial), then reverse the
+    // words -- alpha(Sig(x)^-1 [x] I) = alpha(I) [x] exp(-z_0) [x] ... [x] exp(-z_{M-1})
+    FwdPlan pl;
+    sig_status_t st = make_fwd_plan(B, L, C, depth, stream, bp, pl);
+    if (st != SIG_OK) return st;
+    if (B == 0) return ok();
+    const size_t need = sig_signature_ex_workspace_size(B, L, C, depth, stream, bp, inverse, initial != nullptr);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    if (!out) return fail(SIG_ERR_INVALID_ARG, "out must be non-null");
+    const TensorDims d = make_dims((int)C, depth);
+    const float* ia = nullptr;
+    if (initial) {
+        float* t = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(pl.ws_bytes));
+        cudaError_t e = launch_word_reverse(d, initial, d.S, t, d.S, B, (cudaStream_t)s);
+        if (e != cudaSuccess) return cuda_status(e, "word reversal launch");
+        ia = t;
+    }
+    st = run_signature(path, B, L, C, depth, stream, bp, basepoint, out, ws, pl.ws_bytes, (cudaStream_t)s, -1.0f, ia);
+    if (st != SIG_OK) return st;
+    const int64_t rows = stream ? B * pl.M : B;
+    cudaError_t e = launch_word_reverse(d, out, d.S, out, d.S, rows, (cudaStream_t)s);
+    return cuda_status(e, "word reversal launch");
+}
+
+size_t sig_signature_backward_ex_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
+                                                sig_basepoint_t bp, int32_t inverse, int32_t has_initial,
+                                                int32_t want_grad_initial) {
+    FwdPlan pl;
+    if (make_fwd_plan(B, L, C, depth, stream, bp, pl) != SIG_OK) return 0;
+    if (!inverse) return 0;
+    const int64_t rows = stream ? B * pl.M : B;
+    const size_t S = (size_t)sig_channels_checked(C, depth);
+    return ((size_t)rows * S + (size_t)B * S * (1 + (has_initial ? 1 : 0) + (want_grad_initial ? 1 : 0))) *
+           sizeof(float);
+}
+
+sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path, const float* out_saved, int64_t B,
+                                       int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
+                                       const float* basepoint, int32_t inverse, const float* initial,
+                                       float* grad_path, float* grad_basepoint, float* grad_initial, void* ws,
+                                       size_t ws_bytes, sig_cuda_stream_t s) {
     FwdPlan pl;
     sig_status_t st = make_fwd_plan(B, L, C, depth, stream, bp, pl);
     if (st != SIG_OK) return st;
@@ -383,11 +448,22 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
     if (!grad_out || !path || !out_saved || !grad_path)
         return fail(SIG_ERR_INVALID_ARG, "grad_out, path, out_saved and grad_path must be non-null");
     if (bp == SIG_BP_GIVEN && !basepoint) return fail(SIG_ERR_INVALID_ARG, "basepoint is NULL with SIG_BP_GIVEN");
+    const size_t need = sig_signature_backward_ex_workspace_size(B, L, C, depth, stream, bp, inverse,
+                                                                 initial != nullptr, grad_initial != nullptr);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    const TensorDims d = make_dims((int)C, depth);
+    const int64_t S = d.S;
+    const int64_t rows = stream ? B * pl.M : B;
+    // the forward's final state of each path: its last output row
+    const float* fin = stream ? out_saved + (size_t)(pl.M - 1) * S : out_saved;
+    const int64_t fin_stride = stream ? pl.M * S : S;
     BwdParams prm{};
     prm.grad_out = grad_out;
     prm.path = path;
     prm.basepoint = basepoint;
-    prm.sig_final = out_saved;
+    prm.sig_final = fin;
+    prm.sf_stride = fin_stride;
     prm.bp_mode = (int)bp;
     prm.stream = stream ? 1 : 0;
     prm.B = B;
@@ -395,12 +471,53 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
     prm.M = pl.M;
     prm.grad_path = grad_path;
     prm.grad_bp = (bp == SIG_BP_GIVEN) ? grad_basepoint : nullptr;
-    cudaError_t e = pl.ks->bwd(prm, (cudaStream_t)s);
+    prm.zsign = 1.0f;
+    prm.initial = initial;
+    prm.grad_initial = grad_initial;
+    float* gi_alpha = nullptr;
+    cudaStream_t cs = (cudaStream_t)s;
+    if (inverse) {
+        // the forward scanned the negated path from alpha(initial) and reversed the words of its
+        // output (reading R18): pull every tensor back through alpha, run the scan's VJP, push the
+        // initial's gradient forward through alpha again
+        float* w = static_cast<float*>(ws);
+        float* ga = w;
+        float* sa = ga + (size_t)rows * S;
+        float* ia = sa + (size_t)B * S;
+        float* gia = ia + (initial ? (size_t)B * S : 0);
+        cudaError_t e = launch_word_reverse(d, grad_out, S, ga, S, rows, cs);
+        if (e == cudaSuccess) e = launch_word_reverse(d, fin, fin_stride, sa, S, B, cs);
+        if (e == cudaSuccess && initial) e = launch_word_reverse(d, initial, S, ia, S, B, cs);
+        if (e != cudaSuccess) return cuda_status(e, "word reversal launch");
+        prm.grad_out = ga;
+        prm.sig_final = sa;
+        prm.sf_stride = S;
+        prm.zsign = -1.0f;
+        prm.initial = initial ? ia : nullptr;
+        if (grad_initial) {
+            gi_alpha = gia;
+            prm.grad_initial = gia;
+        }
+    }
+    cudaError_t e = pl.ks->bwd(prm, cs);
     if (e == cudaSuccess) count_launch();
     if (e == cudaErrorInvalidConfiguration)
         return fail(SIG_ERR_UNSUPPORTED, "path of %lld increments does not fit the backward's shared memory",
                     (long long)pl.M);
-    return cuda_status(e, "signature backward launch");
+    if (e != cudaSuccess) return cuda_status(e, "signature backward launch");
+    if (gi_alpha) {
+        e = launch_word_reverse(d, gi_alpha, S, grad_initial, S, B, cs);
+        if (e != cudaSuccess) return cuda_status(e, "word reversal launch");
+    }
+    return ok();
+}
+
+sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
+                                    int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
+                                    const float* basepoint, float* grad_path, float* grad_basepoint,
+                                    sig_cuda_stream_t s) {
+    return sig_signature_backward_ex(grad_out, path, out_saved, B, L, C, depth, stream, bp, basepoint, 0, nullptr,
+                                     grad_path, grad_basepoint, nullptr, nullptr, 0, s);
 }
 
 sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, int64_t C, int32_t depth, float* out,

@@ -109,6 +109,37 @@ __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restr
     }
 }
 
+
+// ---------------------------------------------------------------- word reversal alpha
+// alpha(x)[a_1 .. a_k] = x[a_k .. a_1] on every level: the anti-automorphism with
+// alpha(A [x] B) = alpha(B) [x] alpha(A) and alpha(exp(z)) = exp(z), used for the inverse option
+// (R18).  Row r of in (stride si) -> row r of out (stride so); in == out permutes in place
+// (each pair {w, rev(w)} is swapped by the thread holding the smaller index).
+__global__ void word_reverse_kernel(const TensorDims d, const float* in, int64_t si, float* out, int64_t so,
+                                    int64_t rows) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * d.S) return;
+    const int64_t r = e / d.S;
+    const int f = (int)(e - r * d.S);
+    const int k = level_of(d, f);
+    int w = f - d.off[k], rev = 0;
+    for (int q = 0; q < k; ++q) {
+        const int w2 = (d.C == 1) ? w : (int)__umulhi((uint32_t)w, d.magic);
+        rev = rev * d.C + (w - w2 * d.C);
+        w = w2;
+    }
+    const int g = d.off[k] + rev;
+    if (in == out) {
+        if (g > f) {
+            float* row = out + r * so;
+            const float t = row[f];
+            row[f] = row[g];
+            row[g] = t;
+        }
+    } else {
+        out[r * so + g] = in[r * si + f];
+    }
+}
 #endif  // SIG_DEFINE_COMBINE_KERNELS
 
 // ---------------------------------------------------------------- ordered group fold in smem

@@ -40,6 +40,10 @@ struct BwdParams {
     int64_t B, L, M;
     float* grad_path;        // [B, L, C]
     float* grad_bp;          // [B, C] or nullptr
+    int64_t sf_stride;       // floats between consecutive paths' final states in sig_final
+    float zsign;             // +1, or -1: the forward scanned the negated path (inverse option)
+    const float* initial;    // [B, S] start state of the forward scan, or nullptr (identity)
+    float* grad_initial;     // [B, S] gradient w.r.t. initial, or nullptr
 };
 
 template <class SH>
@@ -60,7 +64,7 @@ struct BwdLayout {
     static size_t smem_bytes(int64_t M) {
         const size_t zf = (size_t)((M * C + 3) / 4 * 4);
         const size_t T = (size_t)tile(M);
-        return (zf + T * RECS * REC + T * C + 32) * sizeof(float);
+        return (zf + T * RECS * REC + T * C + 32 + (size_t)PL * NT) * sizeof(float);
     }
 };
 
@@ -165,11 +169,12 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     float* part = zbuf + (M * C + 3) / 4 * 4;               // [T][RECS][REC] per-step partials
     float* tot = part + (size_t)T * LY::RECS * LY::REC;     // [T][C] per-step gz totals
     float* gprev = tot + (size_t)T * C;                     // [C] gz of the step processed before
+    float* lowred = gprev + 32;                             // [P-1][NT] low-level partials (grad_initial)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int has_bp = prm.bp_mode != 0;
-    const float* sigrow = prm.sig_final + (STREAM ? ((size_t)bidx * M + (M - 1)) * S : (size_t)bidx * S);
+    const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;  // final state of this path
 
     for (int64_t e = tid; e < M * C; e += blockDim.x) {
         const int64_t s = e / C;
@@ -178,7 +183,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
         const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
         const float x1 = xr[r1 * C + c];
         const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
-        zbuf[e] = x1 - x0;
+        zbuf[e] = prm.zsign * (x1 - x0);
     }
     if (tid < C) gprev[tid] = 0.0f;
 
@@ -248,9 +253,19 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
 #pragma unroll
             for (int q = 0; q < SH::PD; ++q) zp[q] = (P > 0) ? zbuf[t * C + p[q]] : 0.0f;
 
-            // (1) reversibility: A <- A [x] exp(-z) on levels < N; the exact identity at t = 0
+            // (1) reversibility: A <- A [x] exp(-z) on levels < N; the exact start state at t = 0
             if (t > 0) {
                 fused_mulexp<SH, N - 1, true>(A, low, z, zp);
+            } else if (prm.initial != nullptr) {
+                const float* ir = prm.initial + (size_t)bidx * S;
+                static_for<SH::K0, N>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    load_run<SH::own(k), SH::own_off(k)>(A, ir + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
+                });
+                static_for<1, P>([&](auto ic) {
+                    constexpr int i = decltype(ic)::value;
+                    low[i] = ir[SH::lvl_off(i) + prefix / (int)ipow(C, P - i)];
+                });
             } else {
 #pragma unroll
                 for (int q = 0; q < SH::OWNA; ++q) A[q] = 0.0f;
@@ -348,15 +363,40 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             const int64_t t = M - 1 - (n0 + j);
             const float before = (j == 0) ? gprev[c] : tot[(j - 1) * C + c];
             float* gr = grad_row(t + 1);
-            if (gr) gr[c] = tot[j * C + c] - before;  // grad x_{t+1} = gz_t - gz_{t+1}
+            if (gr) gr[c] = prm.zsign * (tot[j * C + c] - before);  // grad x_{t+1} = gz_t - gz_{t+1}
             if (t == 0) {
                 float* g0 = grad_row(0);
-                if (g0) g0[c] = -tot[j * C + c];
+                if (g0) g0[c] = -prm.zsign * tot[j * C + c];
             }
         }
         __syncthreads();
         if (tid < C) gprev[tid] = tot[(tn - 1) * C + tid];
         __syncthreads();
+    }
+    if (prm.grad_initial != nullptr) {
+        // G now holds dL/d(start state): owned levels directly; a level i < P coefficient u is the
+        // fixed-order sum of the partials Ghat_i(p) over the C^(P-i) prefixes p extending u
+        float* gi = prm.grad_initial + (size_t)bidx * S;
+        if (valid) {
+            static_for<SH::K0, N + 1>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                store_run<SH::own(k), SH::own_off(k), false>(gi + SH::lvl_off(k) + (int64_t)prefix * SH::own(k), G);
+            });
+        }
+        static_for<1, P>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            lowred[(i - 1) * LY::NT + tid] = valid ? Gh[i] : 0.0f;
+        });
+        __syncthreads();
+        static_for<1, P>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            constexpr int bs = (int)ipow(C, P - i);
+            for (int u = tid; u < (int)ipow(C, i); u += blockDim.x) {
+                float sum = 0.0f;
+                for (int q = 0; q < bs; ++q) sum += lowred[(i - 1) * LY::NT + u * bs + q];
+                gi[SH::lvl_off(i) + u] = sum;
+            }
+        });
     }
 }
 

@@ -34,6 +34,8 @@ struct FwdParams {
                              //      path and writes their ordered product to out + (u / upc) * S
     TensorDims dims;         // level tables for the in-CTA fold (upc > 0)
     float* out;              // stream: [B, M, S]; upc = 0: unit u -> out + u * S
+    float zsign;             // +1, or -1: scan the negated path (the inverse option, R18)
+    const float* initial;    // [B, S] start state of each path's first chunk, or nullptr (identity)
 };
 
 // Depth-first walk of the thread's word tree for the level-K Horner chain (eq-fusedterm):
@@ -140,6 +142,19 @@ __device__ __forceinline__ void store_state(float* row, int prefix, const float 
     });
 }
 
+// Read a state row into the thread's registers (the inverse of store_state).
+template <class SH>
+__device__ __forceinline__ void load_state(const float* row, int prefix, float (&own)[SH::OWN], float (&low)[SH::LOWA]) {
+    static_for<SH::K0, SH::N + 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        load_run<SH::own(k), SH::own_off(k)>(own, row + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
+    });
+    static_for<1, SH::P>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        low[i] = row[SH::lvl_off(i) + prefix / (int)ipow(SH::C, SH::P - i)];
+    });
+}
+
 template <class SH>
 __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     constexpr int C = SH::C;
@@ -169,6 +184,8 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     for (int i = 0; i < SH::OWN; ++i) own[i] = 0.0f;
 #pragma unroll
     for (int i = 0; i < SH::LOWA; ++i) low[i] = 0.0f;
+    // the update case: the path's first chunk starts from the given signature
+    if (prm.initial != nullptr && valid && j == 0) load_state<SH>(prm.initial + (size_t)b * SH::S, prefix, own, low);
 
     for (int64_t t0 = 0; t0 < prm.chunk_len; t0 += T) {
         __syncthreads();
@@ -201,7 +218,7 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
                     float x0;
                     if (g0 >= bb * prm.L * C) x0 = __ldg(xb + g0);
                     else x0 = (prm.bp_mode == 2) ? prm.basepoint[bb * C + c] : 0.0f;
-                    zv = x1 - x0;
+                    zv = prm.zsign * (x1 - x0);
                 }
                 zu[t * C + zswz(C, c)] = zv;  // pair-swapped staging when enabled (see zswz)
             }
