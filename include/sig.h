@@ -192,6 +192,43 @@ sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad
                                        sig_basepoint_t bp, const float* basepoint, float* grad_path,
                                        float* grad_basepoint, void* ws, size_t ws_bytes, sig_cuda_stream_t s);
 
+/* ---------------------------------------------------------------- logsignature of given signatures */
+
+/* K4 / K5 on signature rows already computed (e.g. Path queries, "followed by a log"):
+ *   sig  [rows, S] group-like signatures; out [rows, w] (words / brackets) or [rows, S] (expand)
+ *   grad_sig [rows, S] overwritten; ws >= sig_logsignature_from_signature_workspace_size bytes.
+ * Errors as sig_logsignature. */
+size_t sig_logsignature_from_signature_workspace_size(sig_logsig_plan_t plan, int64_t rows);
+sig_status_t sig_logsignature_from_signature(sig_logsig_plan_t plan, const float* sig, int64_t rows, float* out,
+                                             sig_cuda_stream_t s);
+sig_status_t sig_logsignature_from_signature_backward(sig_logsig_plan_t plan, const float* grad_out, const float* sig,
+                                                      int64_t rows, float* grad_sig, void* ws, size_t ws_bytes,
+                                                      sig_cuda_stream_t s);
+
+/* ---------------------------------------------------------------- Path: O(1) interval queries */
+
+/* P:L171-185 (algorithmic-path): with the prefix signatures and prefix inverse signatures of a
+ * stream precomputed (sig_signature / sig_signature_ex with stream = 1, inverse = 0 / 1: row r is
+ * Sig(x_0 .. x_{r+1}) resp. its inverse, M = number of points - 1), the signature of any interval
+ *     Sig(x_s, .., x_{e-1}) = InvertSig(x_0 .. x_s) [x] Sig(x_0 .. x_{e-1})
+ * is one [x] per query, independent of its length.
+ *   prefix_sig, prefix_inv [B, M, S] (device); starts, ends: Q HOST int64 arrays, 0 <= s,
+ *   s + 2 <= e <= M + 1 (half-open point ranges of >= 2 points; with a basepoint the indices count
+ *   the augmented points); out [B, Q, S] (device).  ws: sig_path_query_workspace_size(M, Q) bytes
+ *   (device copies of the indices; the host arrays may be freed when the call returns).
+ * Backward: grad_prefix_sig / grad_prefix_inv [B, M, S] overwritten with the sums, in ascending
+ * query order (deterministic, no atomics), of the [x]-VJPs of the queries reading each row.
+ * SHAPE for a query outside the stream (checked before any launch).  The paper's caution applies:
+ * numerically unstable for long prefixes. */
+size_t sig_path_query_workspace_size(int64_t M, int64_t Q);
+sig_status_t sig_path_query(const float* prefix_sig, const float* prefix_inv, int64_t B, int64_t M, int64_t C,
+                            int32_t depth, const int64_t* starts, const int64_t* ends, int64_t Q, float* out, void* ws,
+                            size_t ws_bytes, sig_cuda_stream_t s);
+sig_status_t sig_path_query_backward(const float* grad_out, const float* prefix_sig, const float* prefix_inv,
+                                     int64_t B, int64_t M, int64_t C, int32_t depth, const int64_t* starts,
+                                     const int64_t* ends, int64_t Q, float* grad_prefix_sig, float* grad_prefix_inv,
+                                     void* ws, size_t ws_bytes, sig_cuda_stream_t s);
+
 #ifdef __cplusplus
 }
 #endif

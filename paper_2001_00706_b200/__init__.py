@@ -18,6 +18,7 @@ import ctypes
 import os
 import threading
 
+import numpy as np
 import torch
 
 __all__ = [
@@ -90,6 +91,15 @@ def lib():
                                                     _vp, _c_sz, _vp]),
                 ("sig_logsignature_backward", ctypes.c_int, [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _c_i32, ctypes.c_int,
                                                              _vp, _vp, _vp, _vp, _c_sz, _vp]),
+                ("sig_logsignature_from_signature_workspace_size", _c_sz, [_vp, _c_i64]),
+                ("sig_logsignature_from_signature", ctypes.c_int, [_vp, _vp, _c_i64, _vp, _vp]),
+                ("sig_logsignature_from_signature_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _vp, _vp, _c_sz,
+                                                                            _vp]),
+                ("sig_path_query_workspace_size", _c_sz, [_c_i64, _c_i64]),
+                ("sig_path_query", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _c_i64, _vp,
+                                                  _vp, _c_sz, _vp]),
+                ("sig_path_query_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp,
+                                                           _c_i64, _vp, _vp, _vp, _c_sz, _vp]),
             ]
             for name, res, args in sig:
                 fn = getattr(L, name)
@@ -398,3 +408,163 @@ def multi_signature_combine(sigs, C: int, depth: int) -> torch.Tensor:
     if isinstance(sigs, (list, tuple)):
         sigs = torch.stack(list(sigs))
     return sig_multi_signature_combine(sigs, C, depth)
+
+
+# ------------------------------------------------------------------------------------------------
+# logsignature of given signatures, and Path
+# ------------------------------------------------------------------------------------------------
+def sig_logsignature_from_signature(sig, C: int, depth: int, mode: str = "words"):
+    sig = _dev_f32(sig, "sig")
+    S = sig_signature_channels(C, depth)
+    rows = sig.numel() // S
+    plan = LogSigPlan.get(C, depth, mode, sig.device)
+    out = torch.empty(tuple(sig.shape[:-1]) + (plan.width,), device=sig.device, dtype=torch.float32)
+    _check(lib().sig_logsignature_from_signature(plan.handle, _ptr(sig), rows, _ptr(out), _stream(sig.device)),
+           "sig_logsignature_from_signature")
+    return out
+
+
+def sig_logsignature_from_signature_backward(grad_out, sig, C: int, depth: int, mode: str = "words"):
+    sig = _dev_f32(sig, "sig")
+    grad_out = _dev_f32(grad_out, "grad_out")
+    S = sig_signature_channels(C, depth)
+    rows = sig.numel() // S
+    plan = LogSigPlan.get(C, depth, mode, sig.device)
+    Lib = lib()
+    wsb = Lib.sig_logsignature_from_signature_workspace_size(plan.handle, rows)
+    ws = torch.empty(wsb, device=sig.device, dtype=torch.uint8) if wsb else None
+    gs = torch.empty_like(sig)
+    _check(Lib.sig_logsignature_from_signature_backward(plan.handle, _ptr(grad_out), _ptr(sig), rows, _ptr(gs),
+                                                        _ptr(ws), wsb, _stream(sig.device)),
+           "sig_logsignature_from_signature_backward")
+    return gs
+
+
+class _SigToLogsig(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, sig, C, depth, mode):
+        ctx.save_for_backward(sig)
+        ctx.C, ctx.depth, ctx.mode = C, depth, mode
+        return sig_logsignature_from_signature(sig, C, depth, mode)
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (sig,) = ctx.saved_tensors
+        return sig_logsignature_from_signature_backward(grad_out.contiguous(), sig, ctx.C, ctx.depth, ctx.mode), \
+            None, None, None
+
+
+def signature_to_logsignature(sig, C: int, depth: int, mode: str = "words"):
+    """Logsignature of given signature rows [..., S] (K4; differentiable through K5)."""
+    return _SigToLogsig.apply(sig, C, depth, mode)
+
+
+def _queries(starts, ends):
+    qs = np.ascontiguousarray(np.asarray(starts, dtype=np.int64).reshape(-1))
+    qe = np.ascontiguousarray(np.asarray(ends, dtype=np.int64).reshape(-1))
+    if qs.shape != qe.shape:
+        raise ValueError("starts and ends must have the same length")
+    return qs, qe
+
+
+def sig_path_query(prefix_sig, prefix_inv, C: int, depth: int, starts, ends):
+    prefix_sig = _dev_f32(prefix_sig, "prefix_sig")
+    prefix_inv = _dev_f32(prefix_inv, "prefix_inv")
+    B, M, S = prefix_sig.shape
+    qs, qe = _queries(starts, ends)
+    Q = qs.shape[0]
+    Lib = lib()
+    out = torch.empty((B, Q, S), device=prefix_sig.device, dtype=torch.float32)
+    wsb = Lib.sig_path_query_workspace_size(M, Q)
+    ws = torch.empty(wsb, device=prefix_sig.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_path_query(_ptr(prefix_sig), _ptr(prefix_inv), B, M, C, depth, qs.ctypes.data_as(_vp),
+                              qe.ctypes.data_as(_vp), Q, _ptr(out), _ptr(ws), wsb, _stream(prefix_sig.device)),
+           "sig_path_query")
+    return out
+
+
+def sig_path_query_backward(grad_out, prefix_sig, prefix_inv, C: int, depth: int, starts, ends):
+    prefix_sig = _dev_f32(prefix_sig, "prefix_sig")
+    prefix_inv = _dev_f32(prefix_inv, "prefix_inv")
+    grad_out = _dev_f32(grad_out, "grad_out")
+    B, M, S = prefix_sig.shape
+    qs, qe = _queries(starts, ends)
+    Q = qs.shape[0]
+    Lib = lib()
+    gs = torch.empty_like(prefix_sig)
+    gi = torch.empty_like(prefix_inv)
+    wsb = Lib.sig_path_query_workspace_size(M, Q)
+    ws = torch.empty(wsb, device=prefix_sig.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_path_query_backward(_ptr(grad_out), _ptr(prefix_sig), _ptr(prefix_inv), B, M, C, depth,
+                                       qs.ctypes.data_as(_vp), qe.ctypes.data_as(_vp), Q, _ptr(gs), _ptr(gi),
+                                       _ptr(ws), wsb, _stream(prefix_sig.device)), "sig_path_query_backward")
+    return gs, gi
+
+
+class _PathQuery(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, prefix_sig, prefix_inv, C, depth, starts, ends):
+        ctx.save_for_backward(prefix_sig, prefix_inv)
+        ctx.C, ctx.depth, ctx.starts, ctx.ends = C, depth, starts, ends
+        return sig_path_query(prefix_sig, prefix_inv, C, depth, starts, ends)
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        ps, pi = ctx.saved_tensors
+        gs, gi = sig_path_query_backward(grad_out.contiguous(), ps, pi, ctx.C, ctx.depth, ctx.starts, ctx.ends)
+        return gs, gi, None, None, None, None
+
+
+class Path:
+    """Signatory's Path: O(L) precomputation -- the prefix signatures and prefix
+    inverse signatures of the stream (K1, stream mode) -- then any interval's signature in O(1)
+    by one [x] (sig_path_query), its logsignature by a log of that (K4), and `update` to append
+    new points (the initial option).  Differentiable w.r.t. the path (and basepoint).
+
+    Indices follow Python slicing over the (augmented, if a basepoint is given) points:
+    signature(start, end) = Sig(x[start:end]), end - start >= 2."""
+
+    def __init__(self, path: torch.Tensor, depth: int, basepoint=None):
+        if path.dim() != 3:
+            raise ValueError("path must be [B, L, C]")
+        self.depth = depth
+        self.channels = path.shape[-1]
+        self._sig = signature(path, depth, stream=True, basepoint=basepoint)
+        self._inv = signature(path, depth, stream=True, basepoint=basepoint, inverse=True)
+        self._last = path[:, -1, :]
+        self._npoints = path.shape[1] + (0 if basepoint is None or basepoint is False else 1)
+
+    def __len__(self) -> int:
+        return self._npoints
+
+    @property
+    def shape(self):
+        return (self._sig.shape[0], self._npoints, self.channels)
+
+    def _norm(self, start, end):
+        n = self._npoints
+        start = 0 if start is None else (start + n if start < 0 else start)
+        end = n if end is None else (end + n if end < 0 else end)
+        return start, end
+
+    def signatures(self, starts, ends) -> torch.Tensor:
+        """[B, Q, S]: Sig(x[starts[q]:ends[q]]) for every query q."""
+        qs, qe = zip(*(self._norm(a, b) for a, b in zip(starts, ends))) if len(starts) else ((), ())
+        return _PathQuery.apply(self._sig, self._inv, self.channels, self.depth, tuple(qs), tuple(qe))
+
+    def signature(self, start=None, end=None) -> torch.Tensor:
+        """[B, S]: Sig(x[start:end])."""
+        return self.signatures([start], [end])[:, 0]
+
+    def logsignature(self, start=None, end=None, mode: str = "words") -> torch.Tensor:
+        return signature_to_logsignature(self.signature(start, end), self.channels, self.depth, mode)
+
+    def update(self, new_points: torch.Tensor) -> None:
+        """Append points [B, L', C]: extends both prefix tensors from their last rows."""
+        last = self._last
+        ns = signature(new_points, self.depth, stream=True, basepoint=last, initial=self._sig[:, -1])
+        ni = signature(new_points, self.depth, stream=True, basepoint=last, inverse=True, initial=self._inv[:, -1])
+        self._sig = torch.cat([self._sig, ns], dim=1)
+        self._inv = torch.cat([self._inv, ni], dim=1)
+        self._last = new_points[:, -1, :]
+        self._npoints += new_points.shape[1]

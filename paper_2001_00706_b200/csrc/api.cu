@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "../../include/sig.h"
 #define SIG_DEFINE_COMBINE_KERNELS
@@ -331,6 +332,70 @@ sig_status_t check_logsig_smem(const LDims& d, int64_t w, bool brackets) {
     if (logsig_fwd_smem(d, (int)w, brackets) > 227 * 1024 || logsig_bwd_smem(d, false) > kMaxSmem)
         return fail(SIG_ERR_UNSUPPORTED, "logsignature of C=%d depth=%d exceeds one CTA's shared memory", d.C, d.N);
     return SIG_OK;
+}
+
+// K4 on `rows` signature rows -> out
+sig_status_t launch_logsig_fwd(const sig_logsig_plan_s* plan, const float* sig, int64_t rows, float* out,
+                               cudaStream_t s) {
+    LogsigParams p{};
+    p.d = make_ldims(plan->C, plan->N);
+    p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
+    p.tb = device_view(plan);
+    p.rows = rows;
+    p.sig = sig;
+    p.out = out;
+    const size_t smem = logsig_fwd_smem(p.d, (int)plan->w, p.mode == 1);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(logsig_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_status(e, "logsig smem attribute");
+    }
+    logsig_fwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, s>>>(p);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "logsig launch");
+}
+
+// K5 on `rows` rows: dL/dlog -> dL/dSig (gsig), glog = [rows, S] scratch of the fallback kernel
+sig_status_t launch_logsig_bwd(const sig_logsig_plan_s* plan, const float* grad_out, const float* sig, int64_t rows,
+                               float* glog, float* gsig, cudaStream_t s) {
+    LogsigParams p{};
+    p.d = make_ldims(plan->C, plan->N);
+    p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
+    p.tb = device_view(plan);
+    p.rows = rows;
+    p.sig = sig;
+    p.gout = grad_out;
+    p.gsig = gsig;
+    p.glog_ws = glog;
+    const size_t smem_owned = logsig_bwd_owned_smem(p.d);
+    if (LogsigBwdLaunch fn = find_logsig_bwd_owned(plan->C, plan->N)) {
+        cudaError_t e = fn(p, s);
+        if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");
+    } else if (smem_owned <= kMaxSmem) {
+        if (smem_owned > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(logsig_bwd_owned_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem_owned);
+            if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
+        }
+        logsig_bwd_owned_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem_owned, s>>>(p);
+    } else {
+        p.gl_smem = logsig_bwd_smem(p.d, true) <= kMaxSmem;
+        const size_t smem = logsig_bwd_smem(p.d, p.gl_smem);
+        if (smem > 48 * 1024) {
+            cudaError_t e =
+                cudaFuncSetAttribute(logsig_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
+        }
+        logsig_bwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, s>>>(p);
+    }
+    count_launch();
+    return cuda_status(cudaGetLastError(), "logsig backward launch");
+}
+
+// host index arrays -> device copies in the workspace (pageable source: the copy is staged before
+// cudaMemcpyAsync returns, so the host arrays may go away afterwards)
+cudaError_t upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
 }
 
 }  // namespace
@@ -666,21 +731,7 @@ sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t
     float* sig = sig_saved ? sig_saved : reinterpret_cast<float*>(wsb + pl.ws_bytes);
     st = run_signature(path, B, L, plan->C, plan->N, stream, bp, basepoint, sig, ws, pl.ws_bytes, (cudaStream_t)s);
     if (st != SIG_OK) return st;
-    LogsigParams p{};
-    p.d = make_ldims(plan->C, plan->N);
-    p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
-    p.tb = device_view(plan);
-    p.rows = rows;
-    p.sig = sig;
-    p.out = out;
-    const size_t smem = logsig_fwd_smem(p.d, (int)plan->w, p.mode == 1);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(logsig_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_status(e, "logsig smem attribute");
-    }
-    logsig_fwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, (cudaStream_t)s>>>(p);
-    count_launch();
-    return cuda_status(cudaGetLastError(), "logsig launch");
+    return launch_logsig_fwd(plan, sig, rows, out, (cudaStream_t)s);
 }
 
 sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad_out, const float* path,
@@ -703,41 +754,151 @@ sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad
     char* wsb = static_cast<char*>(ws) + pl.ws_bytes;
     float* glog = reinterpret_cast<float*>(wsb) + (size_t)rows * plan->S;
     float* gsig = glog + (size_t)rows * plan->S;
-    LogsigParams p{};
-    p.d = make_ldims(plan->C, plan->N);
-    p.mode = (plan->mode == SIG_LOGSIG_EXPAND) ? 0 : (plan->mode == SIG_LOGSIG_BRACKETS ? 1 : 2);
-    p.tb = device_view(plan);
-    p.rows = rows;
-    p.sig = sig_saved;
-    p.gout = grad_out;
-    p.gsig = gsig;
-    p.glog_ws = glog;
-    const size_t smem_owned = logsig_bwd_owned_smem(p.d);
-    if (LogsigBwdLaunch fn = find_logsig_bwd_owned(plan->C, plan->N)) {
-        cudaError_t e = fn(p, (cudaStream_t)s);
-        if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");
-    } else if (smem_owned <= kMaxSmem) {
-        if (smem_owned > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(logsig_bwd_owned_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem_owned);
-            if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
-        }
-        logsig_bwd_owned_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem_owned, (cudaStream_t)s>>>(p);
-    } else {
-        p.gl_smem = logsig_bwd_smem(p.d, true) <= kMaxSmem;
-        const size_t smem = logsig_bwd_smem(p.d, p.gl_smem);
-        if (smem > 48 * 1024) {
-            cudaError_t e =
-                cudaFuncSetAttribute(logsig_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return cuda_status(e, "logsig bwd smem attribute");
-        }
-        logsig_bwd_kernel<<<(unsigned)rows, LOGSIG_THREADS, smem, (cudaStream_t)s>>>(p);
-    }
-    count_launch();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_status(e, "logsig backward launch");
+    st = launch_logsig_bwd(plan, grad_out, sig_saved, rows, glog, gsig, (cudaStream_t)s);
+    if (st != SIG_OK) return st;
     return sig_signature_backward(gsig, path, sig_saved, B, L, plan->C, plan->N, stream, bp, basepoint, grad_path,
                                   grad_basepoint, s);
+}
+
+size_t sig_logsignature_from_signature_workspace_size(sig_logsig_plan_t plan, int64_t rows) {
+    if (!plan || rows < 0) return 0;
+    return (size_t)rows * plan->S * sizeof(float);
+}
+
+sig_status_t sig_logsignature_from_signature(sig_logsig_plan_t plan, const float* sig, int64_t rows, float* out,
+                                             sig_cuda_stream_t s) {
+    if (!plan) return fail(SIG_ERR_INVALID_ARG, "plan is NULL");
+    if (rows < 0) return fail(SIG_ERR_SHAPE, "rows < 0");
+    if (rows == 0) return ok();
+    if (!sig || !out) return fail(SIG_ERR_INVALID_ARG, "sig and out must be non-null");
+    return launch_logsig_fwd(plan, sig, rows, out, (cudaStream_t)s);
+}
+
+sig_status_t sig_logsignature_from_signature_backward(sig_logsig_plan_t plan, const float* grad_out, const float* sig,
+                                                      int64_t rows, float* grad_sig, void* ws, size_t ws_bytes,
+                                                      sig_cuda_stream_t s) {
+    if (!plan) return fail(SIG_ERR_INVALID_ARG, "plan is NULL");
+    if (rows < 0) return fail(SIG_ERR_SHAPE, "rows < 0");
+    if (rows == 0) return ok();
+    if (!grad_out || !sig || !grad_sig) return fail(SIG_ERR_INVALID_ARG, "grad_out, sig and grad_sig must be non-null");
+    const size_t need = sig_logsignature_from_signature_workspace_size(plan, rows);
+    if (ws_bytes < need || !ws) return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    return launch_logsig_bwd(plan, grad_out, sig, rows, static_cast<float*>(ws), grad_sig, (cudaStream_t)s);
+}
+
+size_t sig_path_query_workspace_size(int64_t M, int64_t Q) {
+    if (M < 0 || Q < 0) return 0;
+    // starts, ends (int64) + two CSRs (int32: M+1 pointers, Q indices), 256-byte aligned pieces
+    return align256(2 * (size_t)Q * sizeof(int64_t)) + 2 * align256(((size_t)M + 1 + (size_t)Q) * sizeof(int));
+}
+
+static sig_status_t check_queries(int64_t M, const int64_t* starts, const int64_t* ends, int64_t Q) {
+    for (int64_t q = 0; q < Q; ++q) {
+        if (starts[q] < 0 || ends[q] < starts[q] + 2 || ends[q] > M + 1)
+            return fail(SIG_ERR_SHAPE, "query %lld = [%lld, %lld) is not an interval of >= 2 of the %lld points",
+                        (long long)q, (long long)starts[q], (long long)ends[q], (long long)(M + 1));
+    }
+    return SIG_OK;
+}
+
+sig_status_t sig_path_query(const float* prefix_sig, const float* prefix_inv, int64_t B, int64_t M, int64_t C,
+                            int32_t depth, const int64_t* starts, const int64_t* ends, int64_t Q, float* out, void* ws,
+                            size_t ws_bytes, sig_cuda_stream_t s) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || C > 8) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (B < 0 || M < 1 || Q < 0) return fail(SIG_ERR_SHAPE, "B=%lld M=%lld Q=%lld", (long long)B, (long long)M, (long long)Q);
+    if (Q > 0 && (!starts || !ends)) return fail(SIG_ERR_INVALID_ARG, "starts and ends must be non-null");
+    sig_status_t st = check_queries(M, starts, ends, Q);
+    if (st != SIG_OK) return st;
+    if (B == 0 || Q == 0) return ok();
+    if (!prefix_sig || !prefix_inv || !out) return fail(SIG_ERR_INVALID_ARG, "prefix_sig, prefix_inv and out must be non-null");
+    const size_t need = sig_path_query_workspace_size(M, Q);
+    if (ws_bytes < need || !ws) return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    cudaStream_t cs = (cudaStream_t)s;
+    int64_t* qs = static_cast<int64_t*>(ws);
+    int64_t* qe = qs + Q;
+    cudaError_t e = upload(qs, starts, Q * sizeof(int64_t), cs);
+    if (e == cudaSuccess) e = upload(qe, ends, Q * sizeof(int64_t), cs);
+    if (e != cudaSuccess) return cuda_status(e, "query upload");
+    PathQueryParams p{};
+    p.d = make_dims((int)C, depth);
+    p.sig = prefix_sig;
+    p.inv = prefix_inv;
+    p.B = B;
+    p.M = M;
+    p.Q = Q;
+    p.qs = qs;
+    p.qe = qe;
+    p.out = out;
+    const int64_t n = B * Q * S;
+    path_query_kernel<<<(unsigned)((n + 255) / 256), 256, 0, cs>>>(p);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "path query launch");
+}
+
+sig_status_t sig_path_query_backward(const float* grad_out, const float* prefix_sig, const float* prefix_inv,
+                                     int64_t B, int64_t M, int64_t C, int32_t depth, const int64_t* starts,
+                                     const int64_t* ends, int64_t Q, float* grad_prefix_sig, float* grad_prefix_inv,
+                                     void* ws, size_t ws_bytes, sig_cuda_stream_t s) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || C > 8) return fail(SIG_ERR_INVALID_ARG, "bad C=%lld depth=%d", (long long)C, depth);
+    if (B < 0 || M < 1 || Q < 0) return fail(SIG_ERR_SHAPE, "B=%lld M=%lld Q=%lld", (long long)B, (long long)M, (long long)Q);
+    if (Q > 0 && (!starts || !ends)) return fail(SIG_ERR_INVALID_ARG, "starts and ends must be non-null");
+    sig_status_t st = check_queries(M, starts, ends, Q);
+    if (st != SIG_OK) return st;
+    if (B == 0) return ok();
+    if (!prefix_sig || !prefix_inv || !grad_prefix_sig || !grad_prefix_inv || (Q > 0 && !grad_out))
+        return fail(SIG_ERR_INVALID_ARG, "tensor pointers must be non-null");
+    const size_t need = sig_path_query_workspace_size(M, Q);
+    if (ws_bytes < need || !ws) return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    // CSRs row -> queries (ascending), built on the host: the sums over queries then have a fixed order
+    std::vector<int> sp(M + 1, 0), ip(M + 1, 0), sq(Q), iq(Q);
+    int64_t ni = 0;
+    for (int64_t q = 0; q < Q; ++q) {
+        ++sp[ends[q] - 2 + 1];
+        if (starts[q] > 0) ++ip[starts[q] - 1 + 1], ++ni;
+    }
+    for (int64_t r = 0; r < M; ++r) sp[r + 1] += sp[r], ip[r + 1] += ip[r];
+    {
+        std::vector<int> fs(sp.begin(), sp.end() - 1), fi(ip.begin(), ip.end() - 1);
+        for (int64_t q = 0; q < Q; ++q) {
+            sq[fs[ends[q] - 2]++] = (int)q;
+            if (starts[q] > 0) iq[fi[starts[q] - 1]++] = (int)q;
+        }
+    }
+    cudaStream_t cs = (cudaStream_t)s;
+    char* w = static_cast<char*>(ws);
+    int64_t* qs = reinterpret_cast<int64_t*>(w);
+    int64_t* qe = qs + Q;
+    int* csr_s = reinterpret_cast<int*>(w + align256(2 * (size_t)Q * sizeof(int64_t)));
+    int* csr_i = reinterpret_cast<int*>(reinterpret_cast<char*>(csr_s) + align256(((size_t)M + 1 + Q) * sizeof(int)));
+    cudaError_t e = upload(qs, starts, Q * sizeof(int64_t), cs);
+    if (e == cudaSuccess) e = upload(qe, ends, Q * sizeof(int64_t), cs);
+    if (e == cudaSuccess) e = upload(csr_s, sp.data(), (M + 1) * sizeof(int), cs);
+    if (e == cudaSuccess) e = upload(csr_s + M + 1, sq.data(), Q * sizeof(int), cs);
+    if (e == cudaSuccess) e = upload(csr_i, ip.data(), (M + 1) * sizeof(int), cs);
+    if (e == cudaSuccess) e = upload(csr_i + M + 1, iq.data(), ni * sizeof(int), cs);
+    if (e != cudaSuccess) return cuda_status(e, "query upload");
+    PathQueryParams p{};
+    p.d = make_dims((int)C, depth);
+    p.sig = prefix_sig;
+    p.inv = prefix_inv;
+    p.B = B;
+    p.M = M;
+    p.Q = Q;
+    p.qs = qs;
+    p.qe = qe;
+    p.gout = grad_out;
+    p.sig_ptr = csr_s;
+    p.sig_q = csr_s + M + 1;
+    p.inv_ptr = csr_i;
+    p.inv_q = csr_i + M + 1;
+    p.gsig = grad_prefix_sig;
+    p.ginv = grad_prefix_inv;
+    const int64_t n = B * M * S;
+    path_query_bwd_kernel<<<(unsigned)((n + 255) / 256), 256, 0, cs>>>(p);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "path query backward launch");
 }
 
 }  // extern "C"

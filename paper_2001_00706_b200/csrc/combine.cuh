@@ -75,6 +75,31 @@ __global__ void combine_pair_kernel(const TensorDims d, const float* __restrict_
 // ---------------------------------------------------------------- VJP of a [x] b
 //   ga_i[u] = go_i[u] + sum_{k>i} sum_v go_k[u v] b_{k-i}[v]
 //   gb_j[v] = go_j[v] + sum_{k>j} sum_u go_k[u v] a_{k-j}[u]
+// for one coefficient (level i, word u) of the row go; b / a nullptr = the identity
+__device__ __forceinline__ float ga_coef(const TensorDims& d, const float* gor, const float* br, int i, int u) {
+    float acc = gor[d.off[i] + u];
+    if (!br) return acc;
+    for (int k = i + 1; k <= d.N; ++k) {
+        const int nv = d.pw[k - i];
+        const float* gk = gor + d.off[k] + u * nv;
+        const float* bk = br + d.off[k - i];
+        for (int v = 0; v < nv; ++v) acc = fmaf(gk[v], bk[v], acc);
+    }
+    return acc;
+}
+__device__ __forceinline__ float gb_coef(const TensorDims& d, const float* gor, const float* ar, int j, int v) {
+    float acc = gor[d.off[j] + v];
+    if (!ar) return acc;
+    for (int k = j + 1; k <= d.N; ++k) {
+        const int nu = d.pw[k - j];
+        const int stride = d.pw[j];
+        const float* gk = gor + d.off[k] + v;
+        const float* ak = ar + d.off[k - j];
+        for (int uu = 0; uu < nu; ++uu) acc = fmaf(gk[uu * stride], ak[uu], acc);
+    }
+    return acc;
+}
+
 __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restrict__ go, const float* __restrict__ a,
                                         const float* __restrict__ b, float* __restrict__ ga, float* __restrict__ gb) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -83,32 +108,75 @@ __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restr
     const int i = level_of(d, f);
     const int u = f - d.off[i];
     const float* gor = go + r * d.S;
-    const float* ar = a + r * d.S;
-    const float* br = b + r * d.S;
-    if (ga) {
-        float acc = gor[f];
-        for (int k = i + 1; k <= d.N; ++k) {
-            const int nv = d.pw[k - i];
-            const float* gk = gor + d.off[k] + u * nv;
-            const float* bk = br + d.off[k - i];
-            for (int v = 0; v < nv; ++v) acc = fmaf(gk[v], bk[v], acc);
-        }
-        ga[r * d.S + f] = acc;
-    }
-    if (gb) {
-        // f indexes level j = i, word v = u
-        float acc = gor[f];
-        for (int k = i + 1; k <= d.N; ++k) {
-            const int nu = d.pw[k - i];
-            const int stride = d.pw[i];
-            const float* gk = gor + d.off[k] + u;
-            const float* ak = ar + d.off[k - i];
-            for (int uu = 0; uu < nu; ++uu) acc = fmaf(gk[uu * stride], ak[uu], acc);
-        }
-        gb[r * d.S + f] = acc;
-    }
+    if (ga) ga[r * d.S + f] = ga_coef(d, gor, b + r * d.S, i, u);
+    if (gb) gb[r * d.S + f] = gb_coef(d, gor, a + r * d.S, i, u);
 }
 
+// ---------------------------------------------------------------- Path interval queries
+//   Sig(x_s .. x_{e-1}) = InvertSig(x_0 .. x_s) [x] Sig(x_0 .. x_{e-1}): with the
+// stream rows sig[b, r] = Sig(x_0 .. x_{r+1}) and inv[b, r] = its inverse, query q = (s, e) reads
+// inv row s-1 (the identity when s = 0) and sig row e-2.
+struct PathQueryParams {
+    TensorDims d;
+    const float* sig;   // [B, M, S]
+    const float* inv;   // [B, M, S]
+    int64_t B, M, Q;
+    const int64_t* qs;  // [Q] starts (device)
+    const int64_t* qe;  // [Q] ends (device)
+    float* out;         // [B, Q, S]
+    // backward
+    const float* gout;                       // [B, Q, S]
+    const int* sig_ptr; const int* sig_q;    // CSR: sig row r -> the queries reading it (ascending)
+    const int* inv_ptr; const int* inv_q;    // CSR: inv row r -> the queries reading it (ascending)
+    float* gsig;                             // [B, M, S] overwritten
+    float* ginv;                             // [B, M, S] overwritten
+};
+
+__global__ void path_query_kernel(const PathQueryParams p) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int S = p.d.S;
+    if (e >= p.B * p.Q * S) return;
+    const int64_t bq = e / S;
+    const int f = (int)(e - bq * S);
+    const int64_t b = bq / p.Q, q = bq - b * p.Q;
+    const int64_t s0 = p.qs[q], e0 = p.qe[q];
+    const float* sr = p.sig + ((size_t)b * p.M + (e0 - 2)) * S;
+    if (s0 == 0) {
+        p.out[e] = sr[f];
+        return;
+    }
+    const float* ir = p.inv + ((size_t)b * p.M + (s0 - 1)) * S;
+    const int k = level_of(p.d, f);
+    p.out[e] = mul_coef(p.d, ir, sr, k, f - p.d.off[k]);
+}
+
+// dL/d(sig row r) = sum over the queries reading it of the b-side VJP, in ascending query order;
+// dL/d(inv row r) likewise with the a-side VJP (deterministic: no atomics)
+__global__ void path_query_bwd_kernel(const PathQueryParams p) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int S = p.d.S;
+    if (e >= p.B * p.M * S) return;
+    const int64_t br = e / S;
+    const int f = (int)(e - br * S);
+    const int64_t b = br / p.M, r = br - b * p.M;
+    const int i = level_of(p.d, f);
+    const int u = f - p.d.off[i];
+    float acc = 0.0f;
+    for (int t = p.sig_ptr[r]; t < p.sig_ptr[r + 1]; ++t) {
+        const int q = p.sig_q[t];
+        const int64_t s0 = p.qs[q];
+        const float* ar = (s0 == 0) ? nullptr : p.inv + ((size_t)b * p.M + (s0 - 1)) * S;
+        acc += gb_coef(p.d, p.gout + ((size_t)b * p.Q + q) * S, ar, i, u);
+    }
+    p.gsig[e] = acc;
+    acc = 0.0f;
+    for (int t = p.inv_ptr[r]; t < p.inv_ptr[r + 1]; ++t) {
+        const int q = p.inv_q[t];
+        const float* sr = p.sig + ((size_t)b * p.M + (p.qe[q] - 2)) * S;
+        acc += ga_coef(p.d, p.gout + ((size_t)b * p.Q + q) * S, sr, i, u);
+    }
+    p.ginv[e] = acc;
+}
 
 // ---------------------------------------------------------------- word reversal alpha
 // alpha(x)[a_1 .. a_k] = x[a_k .. a_1] on every level: the anti-automorphism with

@@ -61,6 +61,24 @@ def test_validation_before_launch(L):
     assert L.sig_status_string(s) == b"SIG_ERR_INVALID_ARG"  # GIVEN basepoint but NULL
 
 
+def test_path_query_validation_before_launch(L):
+    """Queries outside the stream are rejected on the host (SHAPE), before any device access."""
+    import numpy as np
+    qs = np.array([0, 4], dtype=np.int64)
+    qe = np.array([5, 5], dtype=np.int64)  # [4, 5) is a single point
+    vp = ctypes.c_void_p
+    s = L.sig_path_query(vp(16), vp(16), 2, 9, 3, 4, qs.ctypes.data_as(vp), qe.ctypes.data_as(vp), 2, vp(16),
+                         vp(16), 1 << 20, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_SHAPE"
+    assert b"query 1" in L.sig_last_error()
+    qe = np.array([11, 6], dtype=np.int64)  # 11 > M + 1 = 10 points
+    s = L.sig_path_query(vp(16), vp(16), 2, 9, 3, 4, qs.ctypes.data_as(vp), qe.ctypes.data_as(vp), 2, vp(16),
+                         vp(16), 1 << 20, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_SHAPE"
+    s = L.sig_signature_ex(vp(16), 2, 1, 3, 4, 0, 0, None, 1, None, vp(16), None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_SHAPE"  # inverse: same validation as sig_signature
+
+
 def test_workspace_query(L):
     # a single long path is split into time chunks -> needs workspace; a big batch does not
     assert L.sig_signature_workspace_size(1, 2 ** 22, 3, 6, 0, 0) > 0
