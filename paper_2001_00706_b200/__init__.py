@@ -378,8 +378,13 @@ class _LogSignature(torch.autograd.Function):
 
 
 def logsignature(path: torch.Tensor, depth: int, mode: str = "words", stream: bool = False,
-                 basepoint=None) -> torch.Tensor:
-    """LogSig^depth in the 'words' (default, P:L187-192), 'brackets' or 'expand' basis."""
+                 basepoint=None, inverse: bool = False) -> torch.Tensor:
+    """LogSig^depth in the 'words' (default, P:L187-192), 'brackets' or 'expand' basis.
+    inverse: the logsignature of the inverted signature (of every prefix with
+    stream=True) -- the inverse signature scan (K1) followed by K4, both differentiable."""
+    if inverse:
+        sig = signature(path, depth, stream=stream, basepoint=basepoint, inverse=True)
+        return signature_to_logsignature(sig, path.shape[-1], depth, mode)
     f, t = _bp_args(basepoint)
     return _LogSignature.apply(path, depth, mode, stream, f, t)
 

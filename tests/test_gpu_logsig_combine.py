@@ -157,3 +157,40 @@ def test_logsignature_backward_every_compiled_instance(C, N):
         else:
             err = path_rel_err(got, ref)
         assert err < BWD_TOL, (C, N, mode, err)
+
+
+@pytest.mark.parametrize("mode", ["words", "brackets", "expand"])
+@pytest.mark.parametrize("C,N,B,L,bp", [(3, 4, 2, 12, None), (4, 3, 3, 9, "zero"), (2, 5, 2, 10, "given")])
+def test_logsignature_stream_backward(mode, C, N, B, L, bp):
+    """Stream-mode logsignature (every prefix) forward and backward."""
+    x = brownian_paths(B, L, C, seed=40 + C)
+    bpn = None if bp is None else (True if bp == "zero" else normal((B, C), 41).astype(np.float32))
+    bpt = bpn if not isinstance(bpn, np.ndarray) else _cuda(bpn)
+    w = sb.sig_logsignature_channels(C, N, mode)
+    M = L - 1 + (bp is not None)
+    g = normal((B, M, w), seed=42)
+    xt = _cuda(x).requires_grad_(True)
+    out = sb.logsignature(xt, N, mode, stream=True, basepoint=bpt)
+    got = out.detach().cpu().numpy().reshape(-1, w)
+    # K4 takes the float32 signature rows: against the oracle's log of its own signature rounded
+    # to float32 the bar is 1e-4; against the exact log, short prefixes amplify that rounding
+    # (reading R20), hence 5e-4 end to end
+    sig32 = oracle.signature(x, N, stream=True, basepoint=bpn).astype(np.float32)
+    ref32 = oracle.logsignature_from_signature(sig32.reshape(-1, sig32.shape[-1]), C, N, mode)
+    assert block_rel_err(got, ref32, _blocks(C, N, mode)) < FWD_TOL
+    ref = oracle.logsignature(x, N, mode=mode, stream=True, basepoint=bpn)
+    assert block_rel_err(got, ref.reshape(-1, w), _blocks(C, N, mode)) < 5 * FWD_TOL
+    out.backward(_cuda(g))
+    rg, _ = oracle.logsignature_vjp(g, x, N, mode=mode, stream=True, basepoint=bpn)
+    assert path_rel_err(xt.grad.cpu().numpy(), rg) < BWD_TOL
+
+
+@pytest.mark.parametrize("stream", [False, True])
+def test_logsignature_inverse(stream):
+    """log(Sig^-1): for group-like Sig it is -log(Sig) (expand basis)."""
+    C, N, B, L = 3, 4, 2, 11
+    x = brownian_paths(B, L, C, seed=43)
+    inv = sb.logsignature(_cuda(x), N, "expand", stream=stream, inverse=True).cpu().numpy()
+    ref = -oracle.logsignature(x, N, mode="expand", stream=stream)
+    S = ref.shape[-1]
+    assert level_rel_err(inv.reshape(-1, S), ref.reshape(-1, S), C, N) < FWD_TOL
