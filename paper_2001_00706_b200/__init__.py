@@ -187,16 +187,10 @@ def sig_signature(path: torch.Tensor, depth: int, stream: bool = False, basepoin
 
 
 def sig_signature_backward(grad_out, path, out_saved, depth: int, stream: bool = False, basepoint=None):
-    path = _dev_f32(path, "path")
-    grad_out = _dev_f32(grad_out, "grad_out")
-    out_saved = _dev_f32(out_saved, "out_saved")
-    B, L, C = path.shape
-    bpm, bp = _bp(basepoint, path)
-    gp = torch.empty_like(path)
-    gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
-    _check(lib().sig_signature_backward(_ptr(grad_out), _ptr(path), _ptr(out_saved), B, L, C, depth, int(stream), bpm,
-                                        _ptr(bp), _ptr(gp), _ptr(gbp), _stream(path.device)),
-           "sig_signature_backward")
+    """-> (grad_path, grad_basepoint or None).  Goes through sig_signature_backward_ex with its
+    full workspace, so small batches and long paths use the time-parallel (chunked) backward."""
+    gp, gbp, _ = sig_signature_backward_ex(grad_out, path, out_saved, depth, stream, basepoint,
+                                           want_grad_initial=False)
     return gp, gbp
 
 

@@ -334,6 +334,123 @@ sig_status_t check_logsig_smem(const LDims& d, int64_t w, bool brackets) {
     return SIG_OK;
 }
 
+// ---------------------------------------------------------------- backward time chunks (8(f)1)
+struct BwdChunking {
+    int64_t m = 1, chunk_len = 0;
+};
+
+// Time chunks of the reversible backward.  Required when one path's increments exceed what a CTA
+// stages in shared memory; optional -- only when the caller gave workspace -- when the batch
+// alone cannot fill the SMs (fewer paths than 148: about 8 CTAs per SM, chunks >= 64 steps).
+// Stream mode is never chunked (every output row feeds the gradient of all earlier steps).
+bool bwd_chunking(const FwdPlan& pl, int64_t B, int32_t stream, bool may_chunk, BwdChunking& ch) {
+    const int64_t maxc = pl.ks->bwd_max_chunk ? pl.ks->bwd_max_chunk() : pl.M;
+    int64_t m = (pl.M + maxc - 1) / maxc;
+    if (stream) {
+        ch.m = 1;
+        ch.chunk_len = pl.M;
+        return m <= 1;
+    }
+    if (m > 1 && !may_chunk) return false;
+    if (may_chunk && B > 0 && B < 148) {
+        // ~8 CTAs per SM: small chunks also stage fewer increments, so more of them co-reside
+        int64_t mo = (8 * 148 + B - 1) / B;
+        const int64_t cap = pl.M / 64 > 1 ? pl.M / 64 : 1;
+        if (mo > cap) mo = cap;
+        if (mo > m) m = mo;
+    }
+    ch.chunk_len = (pl.M + m - 1) / m;
+    ch.m = (pl.M + ch.chunk_len - 1) / ch.chunk_len;
+    return true;
+}
+
+size_t bwd_chunk_ws_bytes(const BwdChunking& ch, int64_t B, int64_t S, int64_t C) {
+    if (ch.m <= 1) return 0;
+    const size_t rows = (size_t)B * ch.m;
+    return align256(5 * rows * (size_t)S * sizeof(float)) + align256(rows * (size_t)C * sizeof(float));
+}
+
+// inclusive ordered product along the chunk axis (Hillis-Steele, ceil(log2 m) launches); the last
+// step writes `out`, the others alternate with tmp
+cudaError_t chunk_scan(const TensorDims& d, const float* in, float* out, float* tmp, int64_t B, int64_t m, int suffix,
+                       cudaStream_t s) {
+    int steps = 0;
+    for (int64_t o = 1; o < m; o <<= 1) ++steps;
+    if (steps == 0) return cudaMemcpyAsync(out, in, (size_t)B * m * d.S * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    const int64_t n = B * m * d.S;
+    const float* cur = in;
+    int i = 0;
+    for (int64_t o = 1; o < m; o <<= 1, ++i) {
+        float* dst = ((steps - 1 - i) % 2 == 0) ? out : tmp;
+        chunk_scan_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, cur, dst, B, m, o, suffix);
+        count_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        cur = dst;
+    }
+    return cudaSuccess;
+}
+
+// The time-parallel reversible backward: recompute the chunk signatures (K1), their inclusive
+// prefix and suffix products (K3 steps), the gradient at the end of every chunk, then reverse all
+// chunks at once (K2, one CTA per chunk, each starting from its prefix product) and add the shares
+// of the points two chunks have in common.
+sig_status_t run_bwd_chunked(const FwdPlan& pl, const BwdChunking& ch, BwdParams prm, const TensorDims& d, void* ws,
+                             cudaStream_t s) {
+    const int64_t B = prm.B, m = ch.m, S = d.S, C = d.C;
+    const size_t rows = (size_t)B * m;
+    float* units = static_cast<float*>(ws);
+    float* pin = units + rows * S;
+    float* sfx = pin + rows * S;
+    float* tmp = sfx + rows * S;
+    float* gend = tmp + rows * S;
+    float* edge = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align256(5 * rows * (size_t)S * sizeof(float)));
+    FwdParams f{};
+    f.path = prm.path;
+    f.basepoint = prm.basepoint;
+    f.bp_mode = prm.bp_mode;
+    f.stream = 0;
+    f.B = B;
+    f.L = prm.L;
+    f.M = pl.M;
+    f.chunk_len = ch.chunk_len;
+    f.n_chunks = m;
+    f.n_units = (int64_t)rows;
+    f.upc = 0;
+    f.dims = d;
+    f.out = units;
+    f.zsign = prm.zsign;
+    f.initial = prm.initial;
+    cudaError_t e = pl.ks->fwd0(f, s);
+    if (e != cudaSuccess) return cuda_status(e, "chunk signature launch");
+    count_launch();
+    e = chunk_scan(d, units, pin, tmp, B, m, 0, s);
+    if (e == cudaSuccess) e = chunk_scan(d, units, sfx, tmp, B, m, 1, s);
+    if (e != cudaSuccess) return cuda_status(e, "chunk scan launch");
+    const int64_t n = (int64_t)rows * S;
+    chunk_gend_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, prm.grad_out, sfx, B, m, gend);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_status(e, "chunk gradient launch");
+    prm.n_chunks = m;
+    prm.chunk_len = ch.chunk_len;
+    prm.sig_final = pin;
+    prm.sf_stride = S;
+    prm.grad_out = gend;
+    prm.go_stride = S;
+    prm.chunk_init = pin;
+    prm.edge = edge;
+    e = pl.ks->bwd(prm, s);
+    if (e == cudaErrorInvalidConfiguration)
+        return fail(SIG_ERR_UNSUPPORTED, "backward chunk of %lld increments does not fit", (long long)ch.chunk_len);
+    if (e != cudaSuccess) return cuda_status(e, "signature backward launch");
+    count_launch();
+    const int64_t nf = B * (m - 1) * C;
+    chunk_edge_fixup_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, s>>>(prm.grad_path, edge, B, m, ch.chunk_len, prm.L,
+                                                                          prm.bp_mode != 0, (int)C);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "chunk edge launch");
+}
+
 // K4 on `rows` signature rows -> out
 sig_status_t launch_logsig_fwd(const sig_logsig_plan_s* plan, const float* sig, int64_t rows, float* out,
                                cudaStream_t s) {
@@ -491,12 +608,17 @@ size_t sig_signature_backward_ex_workspace_size(int64_t B, int64_t L, int64_t C,
                                                 sig_basepoint_t bp, int32_t inverse, int32_t has_initial,
                                                 int32_t want_grad_initial) {
     FwdPlan pl;
-    if (make_fwd_plan(B, L, C, depth, stream, bp, pl) != SIG_OK) return 0;
-    if (!inverse) return 0;
-    const int64_t rows = stream ? B * pl.M : B;
+    if (make_fwd_plan(B, L, C, depth, stream, bp, pl) != SIG_OK || !pl.ks->bwd) return 0;
     const size_t S = (size_t)sig_channels_checked(C, depth);
-    return ((size_t)rows * S + (size_t)B * S * (1 + (has_initial ? 1 : 0) + (want_grad_initial ? 1 : 0))) *
-           sizeof(float);
+    size_t inv = 0;
+    if (inverse) {
+        const int64_t rows = stream ? B * pl.M : B;
+        inv = align256(((size_t)rows * S + (size_t)B * S * (1 + (has_initial ? 1 : 0) + (want_grad_initial ? 1 : 0))) *
+                       sizeof(float));
+    }
+    BwdChunking ch;
+    if (!bwd_chunking(pl, B, stream, true, ch)) return inv;
+    return inv + bwd_chunk_ws_bytes(ch, B, (int64_t)S, C);
 }
 
 sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path, const float* out_saved, int64_t B,
@@ -513,12 +635,28 @@ sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path,
     if (!grad_out || !path || !out_saved || !grad_path)
         return fail(SIG_ERR_INVALID_ARG, "grad_out, path, out_saved and grad_path must be non-null");
     if (bp == SIG_BP_GIVEN && !basepoint) return fail(SIG_ERR_INVALID_ARG, "basepoint is NULL with SIG_BP_GIVEN");
-    const size_t need = sig_signature_backward_ex_workspace_size(B, L, C, depth, stream, bp, inverse,
-                                                                 initial != nullptr, grad_initial != nullptr);
-    if (ws_bytes < need || (need > 0 && !ws))
-        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
     const TensorDims d = make_dims((int)C, depth);
     const int64_t S = d.S;
+    // workspace: the alpha images (inverse) first, then the backward's time chunks.  Chunks that
+    // only improve occupancy are used when the caller gave room for them.
+    const size_t inv_bytes =
+        inverse ? align256((((size_t)(stream ? B * pl.M : B)) * S +
+                            (size_t)B * S * (1 + (initial ? 1 : 0) + (grad_initial ? 1 : 0))) * sizeof(float))
+                : 0;
+    BwdChunking ch;
+    const size_t full = sig_signature_backward_ex_workspace_size(B, L, C, depth, stream, bp, inverse,
+                                                                 initial != nullptr, grad_initial != nullptr);
+    const bool roomy = ws != nullptr && ws_bytes >= full;
+    if (!bwd_chunking(pl, B, stream, roomy, ch)) {
+        if (stream)
+            return fail(SIG_ERR_UNSUPPORTED, "stream backward of %lld increments does not fit one CTA's shared memory",
+                        (long long)pl.M);
+        return fail(SIG_ERR_WORKSPACE, "this path needs the time-chunked backward: workspace of %zu bytes needed, "
+                    "%zu given", full, ws_bytes);
+    }
+    const size_t need = inv_bytes + bwd_chunk_ws_bytes(ch, B, S, C);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
     const int64_t rows = stream ? B * pl.M : B;
     // the forward's final state of each path: its last output row
     const float* fin = stream ? out_saved + (size_t)(pl.M - 1) * S : out_saved;
@@ -564,13 +702,22 @@ sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path,
             prm.grad_initial = gia;
         }
     }
-    cudaError_t e = pl.ks->bwd(prm, cs);
-    if (e == cudaSuccess) count_launch();
-    if (e == cudaErrorInvalidConfiguration)
-        return fail(SIG_ERR_UNSUPPORTED, "path of %lld increments does not fit the backward's shared memory",
-                    (long long)pl.M);
-    if (e != cudaSuccess) return cuda_status(e, "signature backward launch");
+    prm.n_chunks = 1;
+    prm.chunk_len = pl.M;
+    prm.go_stride = S;
+    if (ch.m > 1) {
+        st = run_bwd_chunked(pl, ch, prm, d, static_cast<char*>(ws) + inv_bytes, cs);
+        if (st != SIG_OK) return st;
+    } else {
+        cudaError_t e = pl.ks->bwd(prm, cs);
+        if (e == cudaSuccess) count_launch();
+        if (e == cudaErrorInvalidConfiguration)
+            return fail(SIG_ERR_UNSUPPORTED, "path of %lld increments does not fit the backward's shared memory",
+                        (long long)pl.M);
+        if (e != cudaSuccess) return cuda_status(e, "signature backward launch");
+    }
     if (gi_alpha) {
+        cudaError_t e;
         e = launch_word_reverse(d, gi_alpha, S, grad_initial, S, B, cs);
         if (e != cudaSuccess) return cuda_status(e, "word reversal launch");
     }

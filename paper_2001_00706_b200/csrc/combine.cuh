@@ -178,6 +178,52 @@ __global__ void path_query_bwd_kernel(const PathQueryParams p) {
     p.ginv[e] = acc;
 }
 
+// ---------------------------------------------------------------- time-parallel backward
+// chunk signatures S_j of each path, j < m, laid out [B, m, S].
+// One Hillis-Steele step of the inclusive ordered product along j (Chen's identity, eq-grouplike):
+//   prefix:  out[b, j] = in[b, j - o] [x] in[b, j]   (j >= o, else a copy)
+//   suffix:  out[b, j] = in[b, j] [x] in[b, j + o]   (j + o < m, else a copy)
+__global__ void chunk_scan_step_kernel(const TensorDims d, const float* __restrict__ in, float* __restrict__ out,
+                                       int64_t B, int64_t m, int64_t o, int suffix) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= B * m * d.S) return;
+    const int64_t bj = e / d.S;
+    const int f = (int)(e - bj * d.S);
+    const int64_t j = bj % m;
+    const float* row = in + bj * d.S;
+    const int k = level_of(d, f);
+    if (!suffix && j >= o) out[e] = mul_coef(d, in + (bj - o) * d.S, row, k, f - d.off[k]);
+    else if (suffix && j + o < m) out[e] = mul_coef(d, row, in + (bj + o) * d.S, k, f - d.off[k]);
+    else out[e] = row[f];
+}
+
+// gradient at the end of chunk j: Sig = P_{j+1} [x] Q_j with Q_j = S_{j+1} [x] .. [x] S_{m-1}
+// (the inclusive suffix product at j + 1; the identity for the last chunk), so
+// dL/dP_{j+1} = the a-side VJP of that product at gbar[b]
+__global__ void chunk_gend_kernel(const TensorDims d, const float* __restrict__ gbar, const float* __restrict__ sfx,
+                                  int64_t B, int64_t m, float* __restrict__ gend) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= B * m * d.S) return;
+    const int64_t bj = e / d.S;
+    const int f = (int)(e - bj * d.S);
+    const int64_t b = bj / m, j = bj - b * m;
+    const int i = level_of(d, f);
+    gend[e] = ga_coef(d, gbar + b * d.S, (j + 1 < m) ? sfx + (bj + 1) * d.S : nullptr, i, f - d.off[i]);
+}
+
+// the first point of chunk j >= 1 is also the last point of chunk j - 1: add the share chunk j
+// wrote to edge (runs after the chunk backward, in stream order -- deterministic)
+__global__ void chunk_edge_fixup_kernel(float* __restrict__ grad_path, const float* __restrict__ edge, int64_t B,
+                                        int64_t m, int64_t chunk_len, int64_t L, int has_bp, int C) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= B * (m - 1) * C) return;
+    const int64_t bj = e / C;
+    const int c = (int)(e - bj * C);
+    const int64_t b = bj / (m - 1), j = 1 + (bj - b * (m - 1));
+    const int64_t row = j * chunk_len - has_bp;  // augmented point j * chunk_len
+    grad_path[(b * L + row) * C + c] += edge[(b * m + j) * C + c];
+}
+
 // ---------------------------------------------------------------- word reversal alpha
 // alpha(x)[a_1 .. a_k] = x[a_k .. a_1] on every level: the anti-automorphism with
 // alpha(A [x] B) = alpha(B) [x] alpha(A) and alpha(exp(z)) = exp(z), used for the inverse option

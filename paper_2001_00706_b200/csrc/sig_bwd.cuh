@@ -44,6 +44,13 @@ struct BwdParams {
     float zsign;             // +1, or -1: the forward scanned the negated path (inverse option)
     const float* initial;    // [B, S] start state of the forward scan, or nullptr (identity)
     float* grad_initial;     // [B, S] gradient w.r.t. initial, or nullptr
+    // time-parallel backward: CTA u reverses chunk j = u % n_chunks of path
+    // b = u / n_chunks, increments [j * chunk_len, min((j+1) * chunk_len, M)).  n_chunks = 1 is the
+    // plain per-path backward.
+    int64_t n_chunks, chunk_len;
+    int64_t go_stride;       // floats between consecutive units' grad_out rows (non-stream)
+    const float* chunk_init; // [B * n_chunks, S]: start state of chunk j >= 1 is row b * n_chunks + j - 1
+    float* edge;             // [B * n_chunks, C]: chunk j >= 1 writes its first point's share here
 };
 
 template <class SH>
@@ -162,11 +169,14 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     constexpr int HW = LY::HW;
     constexpr int64_t S = SH::S;
     extern __shared__ __align__(16) float sm[];
-    const int64_t M = prm.M;
-    const int64_t bidx = blockIdx.x;
+    const int64_t unit = blockIdx.x;
+    const int64_t bidx = unit / prm.n_chunks;            // path
+    const int64_t jc = unit - bidx * prm.n_chunks;       // time chunk
+    const int64_t s0 = jc * prm.chunk_len;               // its first increment
+    const int64_t M = (prm.chunk_len < prm.M - s0) ? prm.chunk_len : prm.M - s0;  // its increments
     const int T = LY::tile(M);
     float* zbuf = sm;                                       // [M][C] increments
-    float* part = zbuf + (M * C + 3) / 4 * 4;               // [T][RECS][REC] per-step partials
+    float* part = zbuf + (prm.chunk_len * C + 3) / 4 * 4;   // [T][RECS][REC] per-step partials
     float* tot = part + (size_t)T * LY::RECS * LY::REC;     // [T][C] per-step gz totals
     float* gprev = tot + (size_t)T * C;                     // [C] gz of the step processed before
     float* lowred = gprev + 32;                             // [P-1][NT] low-level partials (grad_initial)
@@ -174,10 +184,10 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int has_bp = prm.bp_mode != 0;
-    const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;  // final state of this path
+    const float* sigrow = prm.sig_final + (size_t)unit * prm.sf_stride;  // state after this unit
 
     for (int64_t e = tid; e < M * C; e += blockDim.x) {
-        const int64_t s = e / C;
+        const int64_t s = s0 + e / C;
         const int c = (int)(e % C);
         const float* xr = prm.path + bidx * prm.L * C;
         const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
 #pragma unroll
             for (int q = 0; q < SH::own(k); ++q) G[SH::own_off(k) + q] = 0.0f;
         } else {
-            load_run<SH::own(k), SH::own_off(k)>(G, prm.grad_out + (size_t)bidx * S + SH::lvl_off(k) +
+            load_run<SH::own(k), SH::own_off(k)>(G, prm.grad_out + (size_t)unit * prm.go_stride + SH::lvl_off(k) +
                                                         (int64_t)prefix * SH::own(k));
         }
     });
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
         constexpr int tail = (int)ipow(C, P - i);
         low[i] = sigrow[SH::lvl_off(i) + prefix / tail];
         Gh[i] = (!STREAM && valid && prefix % tail == 0)
-                    ? prm.grad_out[(size_t)bidx * S + SH::lvl_off(i) + prefix / tail]
+                    ? prm.grad_out[(size_t)unit * prm.go_stride + SH::lvl_off(i) + prefix / tail]
                     : 0.0f;
     });
     __syncthreads();
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
         for (int j = 0; j < tn; ++j) {
             const int64_t t = M - 1 - (n0 + j);
             if (STREAM && valid) {
-                const float* gr = prm.grad_out + ((size_t)bidx * M + t) * S;
+                const float* gr = prm.grad_out + ((size_t)bidx * prm.M + s0 + t) * S;  // stream: one chunk
                 static_for<SH::K0, N + 1>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     add_run<SH::own(k), SH::own_off(k)>(G, gr + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
@@ -256,8 +266,9 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             // (1) reversibility: A <- A [x] exp(-z) on levels < N; the exact start state at t = 0
             if (t > 0) {
                 fused_mulexp<SH, N - 1, true>(A, low, z, zp);
-            } else if (prm.initial != nullptr) {
-                const float* ir = prm.initial + (size_t)bidx * S;
+            } else if (jc > 0 || prm.initial != nullptr) {
+                // start state: the product of the earlier chunks, or the user's initial
+                const float* ir = (jc > 0) ? prm.chunk_init + (size_t)(unit - 1) * S : prm.initial + (size_t)bidx * S;
                 static_for<SH::K0, N>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     load_run<SH::own(k), SH::own_off(k)>(A, ir + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
@@ -362,18 +373,22 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             const int j = e / C, c = e % C;
             const int64_t t = M - 1 - (n0 + j);
             const float before = (j == 0) ? gprev[c] : tot[(j - 1) * C + c];
-            float* gr = grad_row(t + 1);
+            float* gr = grad_row(s0 + t + 1);
             if (gr) gr[c] = prm.zsign * (tot[j * C + c] - before);  // grad x_{t+1} = gz_t - gz_{t+1}
             if (t == 0) {
-                float* g0 = grad_row(0);
-                if (g0) g0[c] = -prm.zsign * tot[j * C + c];
+                if (jc == 0) {
+                    float* g0 = grad_row(0);
+                    if (g0) g0[c] = -prm.zsign * tot[j * C + c];
+                } else {  // the point shared with the previous chunk: added by the fix-up kernel
+                    prm.edge[unit * C + c] = -prm.zsign * tot[j * C + c];
+                }
             }
         }
         __syncthreads();
         if (tid < C) gprev[tid] = tot[(tn - 1) * C + tid];
         __syncthreads();
     }
-    if (prm.grad_initial != nullptr) {
+    if (prm.grad_initial != nullptr && jc == 0) {
         // G now holds dL/d(start state): owned levels directly; a level i < P coefficient u is the
         // fixed-order sum of the partials Ghat_i(p) over the C^(P-i) prefixes p extending u
         float* gi = prm.grad_initial + (size_t)bidx * S;
@@ -403,15 +418,27 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
 template <class SH>
 cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
     using LY = BwdLayout<SH>;
-    const size_t smem = LY::smem_bytes(prm.M);
+    const size_t smem = LY::smem_bytes(prm.chunk_len);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto kern = prm.stream ? sig_bwd_kernel<SH, true> : sig_bwd_kernel<SH, false>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<(unsigned)prm.B, LY::NT, smem, st>>>(prm);
+    kern<<<(unsigned)(prm.B * prm.n_chunks), LY::NT, smem, st>>>(prm);
     return cudaGetLastError();
+}
+
+// Longest chunk (in increments) whose staged increments fit one CTA's shared memory.
+template <class SH>
+int64_t bwd_max_chunk() {
+    int64_t lo = 1, hi = 1 << 20;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (BwdLayout<SH>::smem_bytes(mid) <= 227 * 1024) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
 }
 
 }  // namespace sigb200

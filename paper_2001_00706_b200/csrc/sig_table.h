@@ -1,5 +1,6 @@
 // sig_table.h -- dispatch table entries produced by gen_instances.py (one per supported (C, N)).
 #pragma once
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace sigb200 {
@@ -9,12 +10,14 @@ struct BwdParams;
 
 using FwdLaunch = cudaError_t (*)(const FwdParams&, cudaStream_t);
 using BwdLaunch = cudaError_t (*)(const BwdParams&, cudaStream_t);
+using BwdMaxChunk = int64_t (*)();
 
 struct KernelSet {
     int C, N;
     int pf0, pf1, pb;   // prefix lengths of the two forward variants and of the backward (-1: none)
     FwdLaunch fwd0, fwd1;
     BwdLaunch bwd;
+    BwdMaxChunk bwd_max_chunk;  // longest time chunk the backward stages in shared memory
 };
 
 const KernelSet* kernels_c1(int N);

@@ -42,5 +42,17 @@ def main():
     x5 = torch.from_numpy(brownian_paths(1, 2**22, 3, 5)).to(dev)
     print("c5 fwd ms:", t_events(lambda: sb.sig_signature(x5, 6), reps=10))
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def c5_bwd():
+    """c5 path with the time-parallel backward (not a BASELINE metric)."""
+    x5 = torch.from_numpy(brownian_paths(1, 2**22, 3, 5)).to("cuda")
+    g5 = torch.from_numpy(normal((1, 1092), 105)).to("cuda")
+    out = sb.sig_signature(x5, 6)
+    print("c5 bwd ms:", t_events(lambda: sb.sig_signature_backward(g5, x5, out, 6), reps=5))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "c5bwd":
+    c5_bwd()
