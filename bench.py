@@ -346,7 +346,7 @@ class Workload:
                 pass
             nbytes = B * M * self.S * 4 + B * self.L * C * 4  # written prefixes + read path
             ach = nbytes / (seg_ms["fwd"] / 1000) / 1e9
-            return {"bound": "hbm", "kernel": "sig_fwd_kernel (stream=True)", "achieved": ach, "peak": hbm,
+            return {"bound": "hbm", "kernel": "sig_fwd_stream_kernel (stream=True, staged rows + TMA bulk stores)", "achieved": ach, "peak": hbm,
                     "unit": "GB/s", "frac": ach / hbm, "traffic": traffic.get("sig_fwd_kernel"),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel_ms": seg_ms["fwd"]}
         f = alg_flops("fwd", B, M, C, N)

@@ -71,7 +71,7 @@ struct BwdLayout {
     static size_t smem_bytes(int64_t M) {
         const size_t zf = (size_t)((M * C + 3) / 4 * 4);
         const size_t T = (size_t)tile(M);
-        return (zf + T * RECS * REC + T * C + 32 + (size_t)PL * NT) * sizeof(float);
+        return (zf + (T + 1) * RECS * REC + T * C + 32 + (size_t)PL * NT) * sizeof(float);
     }
 };
 
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     const int64_t M = (prm.chunk_len < prm.M - s0) ? prm.chunk_len : prm.M - s0;  // its increments
     const int T = LY::tile(M);
     float* zbuf = sm;                                       // [M][C] increments
-    float* part = zbuf + (prm.chunk_len * C + 3) / 4 * 4;   // [T][RECS][REC] per-step partials
-    float* tot = part + (size_t)T * LY::RECS * LY::REC;     // [T][C] per-step gz totals
+    float* part = zbuf + (prm.chunk_len * C + 3) / 4 * 4;   // [1 + T][RECS][REC] per-step partials
+    float* tot = part + (size_t)(T + 1) * LY::RECS * LY::REC;  // [T][C] per-step gz totals
     float* gprev = tot + (size_t)T * C;                     // [C] gz of the step processed before
     float* lowred = gprev + 32;                             // [P-1][NT] low-level partials (grad_initial)
 
@@ -241,117 +241,187 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
         return prm.grad_path + (bidx * prm.L + r) * C;
     };
 
-    for (int64_t n0 = 0; n0 < M; n0 += T) {
-        const int tn = (int)((M - n0) < T ? (M - n0) : T);
-        for (int j = 0; j < tn; ++j) {
-            const int64_t t = M - 1 - (n0 + j);
-            if (STREAM && valid) {
-                const float* gr = prm.grad_out + ((size_t)bidx * prm.M + s0 + t) * S;  // stream: one chunk
-                static_for<SH::K0, N + 1>([&](auto kc) {
-                    constexpr int k = decltype(kc)::value;
-                    add_run<SH::own(k), SH::own_off(k)>(G, gr + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
-                });
-                static_for<1, P>([&](auto ic) {
-                    constexpr int i = decltype(ic)::value;
-                    constexpr int tail = (int)ipow(C, P - i);
-                    if (prefix % tail == 0) Gh[i] += gr[SH::lvl_off(i) + prefix / tail];
-                });
-            }
-            float z[C], zp[SH::PD];
-#pragma unroll
-            for (int c = 0; c < C; ++c) z[c] = zbuf[t * C + c];
-#pragma unroll
-            for (int q = 0; q < SH::PD; ++q) zp[q] = (P > 0) ? zbuf[t * C + p[q]] : 0.0f;
-
-            // (1) reversibility: A <- A [x] exp(-z) on levels < N; the exact start state at t = 0
-            if (t > 0) {
-                fused_mulexp<SH, N - 1, true>(A, low, z, zp);
-            } else if (jc > 0 || prm.initial != nullptr) {
-                // start state: the product of the earlier chunks, or the user's initial
-                const float* ir = (jc > 0) ? prm.chunk_init + (size_t)(unit - 1) * S : prm.initial + (size_t)bidx * S;
-                static_for<SH::K0, N>([&](auto kc) {
-                    constexpr int k = decltype(kc)::value;
-                    load_run<SH::own(k), SH::own_off(k)>(A, ir + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
-                });
-                static_for<1, P>([&](auto ic) {
-                    constexpr int i = decltype(ic)::value;
-                    low[i] = ir[SH::lvl_off(i) + prefix / (int)ipow(C, P - i)];
-                });
-            } else {
-#pragma unroll
-                for (int q = 0; q < SH::OWNA; ++q) A[q] = 0.0f;
-#pragma unroll
-                for (int q = 0; q < SH::LOWA; ++q) low[q] = 0.0f;
-            }
-
-            // (2)+(3): chains k = 1..N bottom-up
-            float gz[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c) gz[c] = 0.0f;
-            float acc[SH::PL1];
-#pragma unroll
-            for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
-            // chains entirely below P: read Ghat_k, tail from level k
-            static_for<1, P>([&](auto kc) {
-                constexpr int k = decltype(kc)::value;
-                float Bp[SH::PL1];
-                prefix_chain_all<SH, k>(Bp, A, low, zp);
-                low_tail<SH, k, k>(Gh[k], Bp, zp, acc, Gh);
-            });
-            // chains k >= max(P,1): owned levels depth-first, then the low tail from level P
+    // one reversed step t: (1) reversibility A <- A [x] exp(-z) on levels < N (FIRST: the exact start
+    // state at t == 0 instead), (2)+(3) chains k = 1..N bottom-up; leaves gz and the low-level
+    // channel partials acc[i] (channel p_{i-1})
+    auto stream_add = [&](int64_t t) {
+        if (STREAM && valid) {
+            const float* gr = prm.grad_out + ((size_t)bidx * prm.M + s0 + t) * S;  // stream: one chunk
             static_for<SH::K0, N + 1>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                float Bp[SH::PL1];
-                prefix_chain_all<SH, k>(Bp, A, low, zp);
-                float bP;
-                if constexpr (k == P) bP = G[SH::own_off(P)];
-                else bP = vjp_visit<SH, k, P, 0>(Bp[P], G, A, z, gz);
-                if constexpr (P >= 1) low_tail<SH, k, P>(bP, Bp, zp, acc, Gh);
+                add_run<SH::own(k), SH::own_off(k)>(G, gr + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
             });
+            static_for<1, P>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                constexpr int tail = (int)ipow(C, P - i);
+                if (prefix % tail == 0) Gh[i] += gr[SH::lvl_off(i) + prefix / tail];
+            });
+        }
+    };
+    auto load_z = [&](int64_t t, float (&z)[C], float (&zp)[SH::PD]) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) z[c] = zbuf[t * C + c];
+#pragma unroll
+        for (int q = 0; q < SH::PD; ++q) zp[q] = (P > 0) ? zbuf[t * C + p[q]] : 0.0f;
+    };
+    // the exact start state at t == 0: the product of the earlier chunks, the user's initial, or 1
+    auto start_state = [&]() {
+        if (jc > 0 || prm.initial != nullptr) {
+            const float* ir = (jc > 0) ? prm.chunk_init + (size_t)(unit - 1) * S : prm.initial + (size_t)bidx * S;
+            static_for<SH::K0, N>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                load_run<SH::own(k), SH::own_off(k)>(A, ir + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
+            });
+            static_for<1, P>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                low[i] = ir[SH::lvl_off(i) + prefix / (int)ipow(C, P - i)];
+            });
+        } else {
+#pragma unroll
+            for (int q = 0; q < SH::OWNA; ++q) A[q] = 0.0f;
+#pragma unroll
+            for (int q = 0; q < SH::LOWA; ++q) low[q] = 0.0f;
+        }
+    };
+    // (2)+(3): chains k = 1..N bottom-up on the rebuilt state; leaves gz and the low-level channel
+    // partials acc[i] (channel p_{i-1}).  Split in two (k < N, then k = N) so that the caller can
+    // place work in between.
+    auto chains_lower = [&](const float (&z)[C], const float (&zp)[SH::PD], float (&gz)[C], float (&acc)[SH::PL1]) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) gz[c] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
+        // chains entirely below P: read Ghat_k, tail from level k
+        static_for<1, (P < N ? P : N)>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            float Bp[SH::PL1];
+            prefix_chain_all<SH, k>(Bp, A, low, zp);
+            low_tail<SH, k, k>(Gh[k], Bp, zp, acc, Gh);
+        });
+        // chains max(P,1) <= k < N: owned levels depth-first, then the low tail from level P
+        static_for<SH::K0, N>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            float Bp[SH::PL1];
+            prefix_chain_all<SH, k>(Bp, A, low, zp);
+            float bP;
+            if constexpr (k == P) bP = G[SH::own_off(P)];
+            else bP = vjp_visit<SH, k, P, 0>(Bp[P], G, A, z, gz);
+            if constexpr (P >= 1) low_tail<SH, k, P>(bP, Bp, zp, acc, Gh);
+        });
+    };
+    auto chain_top = [&](const float (&z)[C], const float (&zp)[SH::PD], float (&gz)[C], float (&acc)[SH::PL1]) {
+        constexpr int k = N;
+        float Bp[SH::PL1];
+        prefix_chain_all<SH, k>(Bp, A, low, zp);
+        float bP;
+        if constexpr (k == P) bP = G[SH::own_off(P)];
+        else bP = vjp_visit<SH, k, P, 0>(Bp[P], G, A, z, gz);
+        if constexpr (P >= 1) low_tail<SH, k, P>(bP, Bp, zp, acc, Gh);
+    };
 
-            // ---- per-step gz: warp reduction into the tile
-            float* rec = part + (size_t)j * LY::RECS * LY::REC;
-            if constexpr (LY::FAST) {
-                // reduce-scatter over lane bits C/2 .. 1: lane l ends with channel l % C summed
-                // over its group of C lanes
-                float v[C];
+    // per-step gz of tile step j into record slot j + 1 (slot 0: dummy), in three stages so that
+    // the caller can spread them over the next step's arithmetic.  FAST: rv[] holds the
+    // reduce-scatter state (lane l ends with channel l % C summed over its group of C lanes).
+    auto reduce_a = [&](float (&v)[C]) {
+        if constexpr (LY::FAST) {
+            static_for<0, ilog2(C)>([&](auto sc_) {
+                constexpr int m = C >> (decltype(sc_)::value + 1);  // C/2, C/4, .., 1
+                const bool up = (lane & m) != 0;
 #pragma unroll
-                for (int c = 0; c < C; ++c) v[c] = gz[c];
-                static_for<0, ilog2(C)>([&](auto sc_) {
-                    constexpr int m = C >> (decltype(sc_)::value + 1);  // C/2, C/4, .., 1
-                    const bool up = (lane & m) != 0;
+                for (int q = 0; q < m; ++q) {
+                    const float send = up ? v[q] : v[q + m];
+                    const float keep = up ? v[q + m] : v[q];
+                    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                }
+            });
+        }
+    };
+    auto reduce_b = [&](const float (&v)[C], const float (&acc)[SH::PL1]) -> float {
+        float tv = 0.0f;
+        if constexpr (LY::FAST) {
+            tv = v[0];
+            if constexpr (P >= 1) tv += acc[P];  // its channel p_{P-1} is lane % C
+            static_for<1, P>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;  // channel p_{i-1}: constant over the group
+                float gsum = acc[i];
 #pragma unroll
-                    for (int q = 0; q < m; ++q) {
-                        const float send = up ? v[q] : v[q + m];
-                        const float keep = up ? v[q + m] : v[q];
-                        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-                    }
-                });
-                float tv = v[0];
-                if constexpr (P >= 1) tv += acc[P];  // its channel p_{P-1} is lane % C
-                static_for<1, P>([&](auto ic) {
-                    constexpr int i = decltype(ic)::value;  // channel p_{i-1}: constant over the group
-                    float gsum = acc[i];
+                for (int m = 1; m < C; m <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, m);
+                if ((lane % C) == p[i - 1]) tv += gsum;
+            });
+        }
+        return tv;
+    };
+    auto reduce_c = [&](float tv, const float (&v)[C], const float (&acc)[SH::PL1], int j) {
+        float* rec = part + (size_t)(j + 1) * LY::RECS * LY::REC;
+        if constexpr (LY::FAST) {
 #pragma unroll
-                    for (int m = 1; m < C; m <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, m);
-                    if ((lane % C) == p[i - 1]) tv += gsum;
-                });
+            for (int m = C; m < 32; m <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, m);
+            if (lane < C) rec[warp * C + lane] = tv;
+        } else {
+            float* r = rec + (size_t)tid * LY::REC;
 #pragma unroll
-                for (int m = C; m < 32; m <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, m);
-                if (lane < C) rec[warp * C + lane] = tv;
-            } else {
-                float* r = rec + (size_t)tid * LY::REC;
+            for (int c = 0; c < C; ++c) r[c] = valid ? v[c] : 0.0f;
 #pragma unroll
-                for (int c = 0; c < C; ++c) r[c] = valid ? gz[c] : 0.0f;
+            for (int q = 0; q < LY::PL; ++q) r[C + q] = (valid && P > 0) ? acc[q + 1] : 0.0f;
+        }
+    };
+
+    for (int64_t n0 = 0; n0 < M; n0 += T) {
+        const int tn = (int)((M - n0) < T ? (M - n0) : T);
+        // Software pipelining: the gz reduction of step j is issued at the top of step j+1, in the
+        // same basic block as that step's arithmetic, so its shuffle latency overlaps the FMAs
+        // (the reduction is independent of the next step's state).  The step with t == 0 (exact
+        // start state instead of the reversal) is peeled out of the loop to keep the body one
+        // block.  rec slot 0 is a dummy that absorbs the reduction of the zero vector at j = 0.
+        const bool last_tile = n0 + tn == M;  // holds the step t == 0
+        const int jn = last_tile ? tn - 1 : tn;
+        float gz[C], acc[SH::PL1];
 #pragma unroll
-                for (int q = 0; q < LY::PL; ++q) r[C + q] = (valid && P > 0) ? acc[q + 1] : 0.0f;
-            }
+        for (int c = 0; c < C; ++c) gz[c] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
+        for (int j = 0; j < jn; ++j) {
+            const int64_t t = M - 1 - (n0 + j);
+            stream_add(t);
+            float z[C], zp[SH::PD];
+            load_z(t, z, zp);
+            float v[C], ac[SH::PL1];  // previous step's gz, reduced while this step computes
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = gz[c];
+#pragma unroll
+            for (int q = 0; q < SH::PL1; ++q) ac[q] = acc[q];
+            reduce_a(v);
+            fused_mulexp<SH, N - 1, true>(A, low, z, zp);  // (1) reversibility, levels < N
+            const float tv = reduce_b(v, ac);
+            chains_lower(z, zp, gz, acc);
+            reduce_c(tv, v, ac, j - 1);
+            chain_top(z, zp, gz, acc);
+        }
+        if (last_tile) {
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = gz[c];
+            reduce_a(v);
+            reduce_c(reduce_b(v, acc), v, acc, tn - 2);
+            stream_add(0);
+            float z[C], zp[SH::PD];
+            load_z(0, z, zp);
+            start_state();
+            chains_lower(z, zp, gz, acc);
+            chain_top(z, zp, gz, acc);
+        }
+        {
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = gz[c];
+            reduce_a(v);
+            reduce_c(reduce_b(v, acc), v, acc, tn - 1);
         }
         // ---- flush: per-step totals in a fixed order, then the gradient rows
         __syncthreads();
         for (int e = tid; e < tn * C; e += blockDim.x) {
             const int j = e / C, c = e % C;
-            const float* rec = part + (size_t)j * LY::RECS * LY::REC;
+            const float* rec = part + (size_t)(j + 1) * LY::RECS * LY::REC;
             float s = 0.0f;
             if constexpr (LY::FAST) {
                 for (int w = 0; w < HW; ++w) s += rec[w * C + c];

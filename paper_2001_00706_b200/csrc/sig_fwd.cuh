@@ -263,8 +263,183 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     if (valid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Stream mode with staged output (A4): the output [B, M, S] is written once and never
+// read back, so the store path decides the speed.  Each thread owns scattered runs of a row (its
+// prefix blocks), and storing them directly touches every 32-byte sector several times.  Here a CTA
+// holds whole units (paths); every step, its threads write their coefficients into a row image in
+// shared memory, and after OT steps one thread writes the unit's OT consecutive rows -- one
+// contiguous run of global memory -- with a TMA bulk copy (cp.async.bulk, shared -> global).  The
+// run is only 8-byte aligned in general, so the image sits at the same phase mod 16 bytes as its
+// global destination; the 16-byte-aligned interior goes by TMA, the <= 3 floats at each end by
+// plain stores.  Two images per unit alternate, so the copy of one tile overlaps the next tile.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct StreamStage {
+    int nu;       // units (paths) per CTA
+    int ot;       // steps per output image
+    int64_t img;  // floats per image (ot * S + 4, rounded up to 4)
+};
+
+__host__ __device__ inline int64_t stream_img_floats(int ot, int64_t S) { return ((int64_t)ot * S + 4 + 3) / 4 * 4; }
+
+template <class SH>
+__global__ void __launch_bounds__(512, 1) sig_fwd_stream_kernel(const FwdParams prm, const StreamStage sg) {
+    constexpr int C = SH::C;
+    constexpr int64_t S = SH::S;
+    extern __shared__ __align__(16) float sm[];
+    const int nu = sg.nu, OT = sg.ot;
+    const int T = prm.tile;
+    float* zs = sm;                                        // [nu][T][C]
+    float* img = sm + ((int64_t)nu * T * C + 3) / 4 * 4;  // [2][nu][img]
+    const int ul = threadIdx.x / SH::CP;
+    const int prefix = threadIdx.x % SH::CP;
+    const int64_t unit0 = (int64_t)blockIdx.x * nu;
+    const int64_t b = unit0 + ul;
+    const bool valid = ul < nu && b < prm.B;
+    const int has_bp = prm.bp_mode != 0;
+    const int64_t M = prm.M;
+
+    int p[SH::PD];
+    prefix_digits<SH>(prefix, p);
+    float own[SH::OWN];
+    float low[SH::LOWA];
+#pragma unroll
+    for (int i = 0; i < SH::OWN; ++i) own[i] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < SH::LOWA; ++i) low[i] = 0.0f;
+    if (prm.initial != nullptr && valid) load_state<SH>(prm.initial + (size_t)b * S, prefix, own, low);
+
+    // flush image `buf` holding steps [s, s + n) of every unit of the CTA
+    auto flush = [&](int buf, int64_t s, int n) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        for (int u = 0; u < nu; ++u) {
+            const int64_t bb = unit0 + u;
+            if (bb >= prm.B) break;
+            const int64_t g0 = (bb * M + s) * S, g1 = g0 + (int64_t)n * S;
+            const int ph = (int)(g0 & 3);
+            const float* im = img + ((int64_t)buf * nu + u) * sg.img;  // row data at im[ph ..]
+            const int64_t a0 = (g0 + 3) & ~(int64_t)3, a1 = g1 & ~(int64_t)3;
+            if (a1 > a0) {
+                if (threadIdx.x == 0) bulk_s2g(prm.out + a0, im + ph + (a0 - g0), (uint32_t)((a1 - a0) * sizeof(float)));
+                const int e = (int)threadIdx.x - 1;  // edges: threads 1..6
+                if (e >= 0 && e < 3 && g0 + e < a0) prm.out[g0 + e] = im[ph + e];
+                if (e >= 3 && e < 6 && a1 + (e - 3) < g1) prm.out[a1 + (e - 3)] = im[ph + (a1 - g0) + (e - 3)];
+            } else {
+                for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) prm.out[g] = im[ph + (g - g0)];
+            }
+        }
+        if (threadIdx.x == 0) {
+            bulk_commit();
+            bulk_wait_read1();  // the other image (flushed last time) has been read: free to refill
+        }
+        __syncthreads();
+    };
+
+    int buf = 0, fill = 0;  // image being filled, steps in it
+    int64_t fs = 0;         // first step of the image
+    for (int64_t t0 = 0; t0 < M; t0 += T) {
+        __syncthreads();
+        for (int uu = 0; uu < nu; ++uu) {
+            const int64_t bb = unit0 + uu;
+            const int cnt = (bb < prm.B) ? (int)(M - t0 < T ? M - t0 : T) : 0;
+            const int64_t rowbase = (bb * prm.L + (t0 - has_bp)) * C;
+            float* zu = zs + (size_t)uu * T * C;
+            for (int i = threadIdx.x; i < T * C; i += blockDim.x) {
+                const int t = i / C, c = i - (i / C) * C;
+                float zv = 0.0f;
+                if (t < cnt) {
+                    const int64_t g = rowbase + i;
+                    const float x1 = __ldg(prm.path + g + C);
+                    float x0;
+                    if (g >= bb * prm.L * C) x0 = __ldg(prm.path + g);
+                    else x0 = (prm.bp_mode == 2) ? prm.basepoint[bb * C + c] : 0.0f;
+                    zv = prm.zsign * (x1 - x0);
+                }
+                zu[t * C + zswz(C, c)] = zv;
+            }
+        }
+        __syncthreads();
+        const int tl = (int)(M - t0 < T ? M - t0 : T);
+        const float* zrow = zs + (size_t)(valid ? ul : 0) * T * C;
+        for (int t = 0; t < tl; ++t) {
+            float z[C];
+            float zp[SH::PD];
+#pragma unroll
+            for (int c = 0; c < C; ++c) z[c] = zrow[t * C + zswz(C, c)];
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zp[q] = (SH::P > 0) ? zrow[t * C + zswz(C, p[q])] : 0.0f;
+            fused_mulexp<SH, SH::N, false>(own, low, z, zp);
+            if (valid) {
+                const int64_t g0 = (b * M + fs) * S;
+                float* row = img + ((int64_t)buf * nu + ul) * sg.img + (g0 & 3) + (int64_t)fill * S;
+                store_state<SH, false>(row, prefix, own, low);
+            }
+            if (++fill == OT) {
+                flush(buf, fs, fill);
+                buf ^= 1;
+                fs += fill;
+                fill = 0;
+            }
+        }
+    }
+    if (fill > 0) flush(buf, fs, fill);
+    if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <class SH>
+cudaError_t launch_fwd_stream_staged(const FwdParams& prm_in, cudaStream_t st, bool* done) {
+    *done = false;
+    constexpr int64_t S = SH::S;
+    constexpr int CP = SH::CP;
+    if (!prm_in.stream || prm_in.n_chunks != 1 || CP > 512) return cudaSuccess;
+    // units per CTA: enough threads for a few warps, but at least ~2 CTAs per SM
+    int nu = 1;
+    while ((nu * 2) * CP <= 256 && (prm_in.B + nu * 2 - 1) / (nu * 2) >= 2 * 148) nu *= 2;
+    const size_t budget = 100 * 1024;
+    int ot = 16;
+    while (ot > 1 && 2 * (size_t)nu * stream_img_floats(ot, S) * sizeof(float) > budget) ot /= 2;
+    if (2 * (size_t)nu * stream_img_floats(ot, S) * sizeof(float) > budget || ot < 2) return cudaSuccess;
+    FwdParams prm = prm_in;
+    int tile = (int)(prm.M < 256 ? prm.M : 256);
+    while (tile > 8 && (size_t)nu * tile * SH::C * 4 > 16 * 1024) tile /= 2;
+    prm.tile = tile;
+    StreamStage sg{nu, ot, stream_img_floats(ot, S)};
+    const size_t smem = (((size_t)nu * tile * SH::C + 3) / 4 * 4 + 2 * (size_t)nu * sg.img) * sizeof(float);
+    if (smem > 227 * 1024) return cudaSuccess;
+    auto kern = sig_fwd_stream_kernel<SH>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int bd = (nu * CP + 31) / 32 * 32;
+    const int64_t grid = (prm.B + nu - 1) / nu;
+    kern<<<(unsigned)grid, bd, smem, st>>>(prm, sg);
+    *done = true;
+    return cudaGetLastError();
+}
+
 template <class SH>
 cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
+#if !defined(SIG_STREAM_DIRECT)
+    {
+        bool done = false;
+        cudaError_t e = launch_fwd_stream_staged<SH>(prm_in, st, &done);
+        if (e != cudaSuccess || done) return e;
+    }
+#endif
     FwdParams prm = prm_in;
     const int64_t threads = prm.n_units * (int64_t)SH::CP;
     int bd = 512;

@@ -55,7 +55,10 @@ def test_forward_parity(C, N, B, L, kind):
     assert err < FWD_TOL, err
 
 
-@pytest.mark.parametrize("C,N,B,L", [(6, 4, 5, 60), (4, 4, 3, 33), (8, 3, 4, 20), (3, 6, 2, 41)])
+@pytest.mark.parametrize("C,N,B,L", [(6, 4, 5, 60), (4, 4, 3, 33), (8, 3, 4, 20), (3, 6, 2, 41),
+                                     # many units per CTA in the staged stream kernel, odd S (rows
+                                     # at every 4-byte phase), steps not a multiple of the image
+                                     (5, 3, 700, 23), (2, 5, 1300, 14), (3, 2, 900, 3), (7, 3, 301, 40)])
 def test_forward_stream_parity(C, N, B, L):
     x = brownian_paths(B, L, C, seed=7 + C)
     got = sb.sig_signature(_cuda(x), N, stream=True).cpu().numpy()
@@ -172,3 +175,18 @@ def test_c2_full_size_sampled():
     eb = path_rel_err(gp.cpu().numpy()[idx], rg)
     print(f"PARITY c2 full-size sampled: fwd {ef:.3e} bwd {eb:.3e}")
     assert ef < FWD_TOL and eb < BWD_TOL
+
+
+def test_c3_full_size_sampled():
+    """BASELINE config c3 at full size (B=256, L=1024, C=6, N=4, stream=True) in the launch
+    configuration bench.py times (staged rows, TMA bulk stores): every 32nd path checked against the
+    oracle at every step."""
+    C, N, B, L = 6, 4, 256, 1024
+    x = brownian_paths(B, L, C, seed=3)
+    out = sb.sig_signature(_cuda(x), N, stream=True)
+    idx = np.arange(5, B, 32)
+    got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+    ref = oracle.signature(x[idx], N, stream=True, threads=16)
+    err = level_rel_err(got, ref, C, N)
+    print(f"PARITY c3 full-size sampled: {err:.3e}")
+    assert err < FWD_TOL
