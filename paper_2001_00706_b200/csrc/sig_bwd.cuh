@@ -53,6 +53,21 @@ struct BwdParams {
     float* edge;             // [B * n_chunks, C]: chunk j >= 1 writes its first point's share here
 };
 
+// Per-step gz records are flushed every T steps (a CTA barrier each time).  With up to 128 steps
+// per tile a c2/c4 path has a single flush, so the warps run the whole reversal without a barrier.
+#ifndef SIG_BWD_TMAX
+#define SIG_BWD_TMAX 128
+#endif
+#ifndef SIG_BWD_TILE_KB
+#define SIG_BWD_TILE_KB 160
+#endif
+// With two warps per SM sub-partition (the 8-warp CTAs of e.g. C=4, N=7), delaying one of them by
+// about half a step at the start keeps their FMA-dense and latency-bound phases interleaved
+// (measured: c4 backward -5%; with four warps per sub-partition it costs 7%, so it is off there).
+#ifndef SIG_BWD_STAGGER
+#define SIG_BWD_STAGGER 400
+#endif
+
 template <class SH>
 struct BwdLayout {
     static constexpr int C = SH::C, N = SH::N, P = SH::P;
@@ -64,8 +79,8 @@ struct BwdLayout {
     static constexpr int REC = FAST ? C : (C + PL);  // floats per record
     static constexpr int RECS = FAST ? HW : NT;      // records per step
     __host__ __device__ static int tile(int64_t M) {
-        int T = 32;
-        while (T > 1 && (size_t)T * RECS * REC * sizeof(float) > 64 * 1024) T >>= 1;
+        int T = SIG_BWD_TMAX;
+        while (T > 1 && (size_t)T * RECS * REC * sizeof(float) > SIG_BWD_TILE_KB * 1024) T >>= 1;
         return (int)(T < M ? T : M);
     }
     static size_t smem_bytes(int64_t M) {
@@ -231,6 +246,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
                     : 0.0f;
     });
     __syncthreads();
+    if (SIG_BWD_STAGGER > 0 && HW == 8 && ((warp >> 2) & 1)) __nanosleep(SIG_BWD_STAGGER);
 
     auto grad_row = [&](int64_t r) -> float* {
         // augmented point r (r == 0 is the basepoint when one is given)
