@@ -23,15 +23,15 @@ def report(path):
             print(f"  {r[mn]:36s} {r[mv]:>16s} {r[mu]}")
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
-    hh, vv = rr[0], rr[2]
+    hh, uu, vv = rr[0], rr[1], rr[2]
     want = ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
             "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum", "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum",
             "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum")
-    for name, val in zip(hh, vv):
+    for name, unit, val in zip(hh, uu, vv):
         if name in want:
-            print(f"  {name:60s} {val}")
+            print(f"  {name:60s} {val} {unit}")
     stalls = [(n, v) for n, v in zip(hh, vv) if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
     tot = sum(float(v.replace(",", "") or 0) for _, v in stalls) or 1.0
     top = sorted(stalls, key=lambda nv: -float(nv[1].replace(",", "") or 0))[:6]
