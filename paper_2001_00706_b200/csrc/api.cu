@@ -461,6 +461,17 @@ sig_status_t launch_logsig_fwd(const sig_logsig_plan_s* plan, const float* sig, 
     p.rows = rows;
     p.sig = sig;
     p.out = out;
+#if !defined(SIG_LOGSIG_FWD_GENERIC)
+    if (LogsigFwdLaunch fn = find_logsig_fwd_t(plan->C, plan->N)) {
+        cudaError_t e = fn(p, s);
+        if (e == cudaSuccess) {
+            count_launch();
+            return ok();
+        }
+        if (e != cudaErrorInvalidConfiguration) return cuda_status(e, "logsig launch");
+        (void)cudaGetLastError();  // shape too large for the compiled form: the generic kernel below
+    }
+#endif
     const size_t smem = logsig_fwd_smem(p.d, (int)plan->w, p.mode == 1);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(logsig_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -20,7 +20,30 @@ LogsigBwdLaunch pick(int N, std::integer_sequence<int, Ns...>) {
     return r;
 }
 
+template <int C, int N>
+constexpr LogsigFwdLaunch fentry() {
+    if constexpr (LogFwdT<C, N>::HS * 16 + LogFwdT<C, N>::XSP * 4 <= kOwnedMaxSmem) return &launch_logsig_fwd_t<C, N>;
+    else return nullptr;
+}
+
+template <int C, int... Ns>
+LogsigFwdLaunch fpick(int N, std::integer_sequence<int, Ns...>) {
+    LogsigFwdLaunch r = nullptr;
+    ((N == Ns + 1 ? (r = fentry<C, Ns + 1>(), 0) : 0), ...);
+    return r;
+}
+
 }  // namespace
+
+LogsigFwdLaunch find_logsig_fwd_t(int C, int N) {
+    switch (C) {
+        case 1: return fpick<1>(N, std::make_integer_sequence<int, 12>{});
+        case 2: return fpick<2>(N, std::make_integer_sequence<int, 12>{});
+        case 4: return fpick<4>(N, std::make_integer_sequence<int, 7>{});
+        case 8: return fpick<8>(N, std::make_integer_sequence<int, 5>{});
+        default: return nullptr;
+    }
+}
 
 LogsigBwdLaunch find_logsig_bwd_owned(int C, int N) {
     switch (C) {

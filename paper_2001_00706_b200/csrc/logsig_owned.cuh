@@ -306,6 +306,134 @@ cudaError_t launch_logsig_bwd_owned_t(const LogsigParams& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// K4 (logsignature forward) compiled per (C, N), power-of-two C: the same Horner recursion as
+// logsig_fwd_kernel (H_N = 1/N, H_n = 1/n - x H_{n+1} on levels 0..N-n, log = x H_1; reading R7),
+// float64 accumulation of float32 inputs, but every level loop unrolled and every index a shift or
+// mask: (x H)_m[w] = sum_{i=1}^{m} x_i[w >> (m-i) log2 C] * H_{m-i}[w & (C^(m-i) - 1)].
+// H_n lives in one of two float64 buffers (levels 0..N-1); x on levels 1..N-1 in shared memory
+// (the top level is read once from global by the output stage).
+// ---------------------------------------------------------------------------------------------
+template <class T>
+__host__ __device__ constexpr int hofs(int m) {  // offset of level m in an H buffer
+    int s = 0;
+    for (int j = 0; j < m; ++j) s += T::pw(j);
+    return s;
+}
+
+template <class T, int K>
+__device__ __forceinline__ double log_coef_t(const float* xs, const float* srcN, const double* H1, int w) {
+    double acc = 0.0;
+    static_for<1, K + 1>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        float xv;
+        if constexpr (i == T::N) xv = __ldg(srcN + w);
+        else xv = xs[T::off(i) + (w >> (T::LC * (K - i)))];
+        acc = fma((double)xv, H1[hofs<T>(K - i) + (w & (T::pw(K - i) - 1))], acc);
+    });
+    return acc;
+}
+
+template <int C, int N>
+struct LogFwdT {
+    using T = LT<C, N>;
+    static constexpr int HS = hofs<T>(N);              // levels 0..N-1
+    static constexpr int XSP = (T::XS + 3) / 4 * 4;      // x on levels 1..N-1, padded
+    static size_t smem(int w, bool brackets) {
+        return 2 * (size_t)HS * sizeof(double) + (size_t)XSP * sizeof(float) + (brackets ? (size_t)w * sizeof(float) : 0);
+    }
+};
+
+#ifndef SIG_LOGFWD_THREADS
+#define SIG_LOGFWD_THREADS 512
+#endif
+template <int C, int N>
+__global__ void __launch_bounds__(SIG_LOGFWD_THREADS, 1024 / SIG_LOGFWD_THREADS) logsig_fwd_t_kernel(const LogsigParams p) {
+    using T = LT<C, N>;
+    using F = LogFwdT<C, N>;
+    const int64_t row = blockIdx.x;
+    extern __shared__ __align__(16) double lsd[];
+    double* Hbuf[2] = {lsd, lsd + F::HS};
+    float* xs = reinterpret_cast<float*>(lsd + 2 * F::HS);
+    float* psi = xs + F::XSP;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const float* src = p.sig + row * T::S;
+    for (int f = tid; f < T::XS; f += nth) xs[f] = src[f];
+    if (tid == 0) Hbuf[0][0] = 1.0 / (double)N;  // H_N (level 0 only)
+    __syncthreads();
+    // H_n, n = N-1 .. 1, into buffer (N - n) & 1
+    static_for<1, N>([&](auto nc) {
+        constexpr int n = N - decltype(nc)::value;
+        const double* Hc = Hbuf[(N - n - 1) & 1];
+        double* Hn = Hbuf[(N - n) & 1];
+        static_for<0, N - n + 1>([&](auto mc) {
+            constexpr int m = decltype(mc)::value;
+            for (int w = tid; w < T::pw(m); w += nth) {
+                double val = 1.0 / (double)n;
+                if constexpr (m > 0) {
+                    double acc = 0.0;
+                    static_for<1, m + 1>([&](auto ic) {
+                        constexpr int i = decltype(ic)::value;
+                        acc = fma((double)xs[T::off(i) + (w >> (T::LC * (m - i)))],
+                                  Hc[hofs<T>(m - i) + (w & (T::pw(m - i) - 1))], acc);
+                    });
+                    val = -acc;
+                }
+                Hn[hofs<T>(m) + w] = val;
+            }
+        });
+        __syncthreads();
+    });
+    const double* H1 = Hbuf[(N - 1) & 1];
+    const float* srcN = src + T::off(N);
+    if (p.mode == 0) {
+        float* o = p.out + row * T::S;
+        static_for<1, N + 1>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            for (int w = tid; w < T::pw(k); w += nth) o[T::off(k) + w] = (float)log_coef_t<T, k>(xs, srcN, H1, w);
+        });
+        return;
+    }
+    float* o = p.out + row * p.tb.w;
+    for (int j = tid; j < p.tb.w; j += nth) {
+        const int f = (int)p.tb.lyn_idx[j];
+        double v = 0.0;
+        static_for<1, N + 1>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            if (f >= T::off(k) && f < T::off(k + 1)) v = log_coef_t<T, k>(xs, srcN, H1, f - T::off(k));
+        });
+        if (p.mode == 2) o[j] = (float)v;
+        else psi[j] = (float)v;
+    }
+    if (p.mode == 1) {
+        __syncthreads();
+        // exact integer coefficients of (psi o phi)^{-1}
+        for (int r = tid; r < p.tb.w; r += nth) {
+            double acc = 0.0;
+            for (int e = p.tb.minv_rowptr[r]; e < p.tb.minv_rowptr[r + 1]; ++e)
+                acc = fma((double)p.tb.minv_val[e], (double)psi[p.tb.minv_col[e]], acc);
+            o[r] = (float)acc;
+        }
+    }
+}
+
+template <int C, int N>
+cudaError_t launch_logsig_fwd_t(const LogsigParams& p, cudaStream_t st) {
+    const size_t smem = LogFwdT<C, N>::smem(p.tb.w, p.mode == 1);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    if (smem > 48 * 1024) {
+        cudaError_t e =
+            cudaFuncSetAttribute(logsig_fwd_t_kernel<C, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    logsig_fwd_t_kernel<C, N><<<(unsigned)p.rows, SIG_LOGFWD_THREADS, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+using LogsigFwdLaunch = cudaError_t (*)(const LogsigParams&, cudaStream_t);
+// nullptr when (C, N) has no compiled instance
+LogsigFwdLaunch find_logsig_fwd_t(int C, int N);
+
 using LogsigBwdLaunch = cudaError_t (*)(const LogsigParams&, cudaStream_t);
 // nullptr when (C, N) has no compiled instance (non power-of-two C, or too large for one CTA)
 LogsigBwdLaunch find_logsig_bwd_owned(int C, int N);
