@@ -501,8 +501,304 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     }
 }
 
+#ifndef SIG_BWD2_STAGGER
+#define SIG_BWD2_STAGGER 0
+#endif
+// ---------------------------------------------------------------------------------------------
+// K2 with two sibling prefixes per thread ("R = 2").  Everything a thread computes below level P
+// -- the replicated prefix values low[], the prefix-chain values B_i (i < P), the partial
+// low-level gradient Ghat and the low tails of every chain, the C-vector gz -- is the same for the
+// sibling prefixes pa = 2t and pb = 2t + 1 (same p[:P-1]); only level P and above differ.  One
+// thread therefore carries both blocks and does the shared work once: per useful FMA this halves
+// the scalar overhead and the gz reduction.  Half the threads (CP/2 per path) with twice the
+// registers (up to 255): two warps per SM sub-partition instead of four.
+// Used for plain calls (no stream, no time chunks, no initial state) of shapes with even C, P >= 2
+// and CP/2 a multiple of 32 (BwdLayout2::OK); everything else runs sig_bwd_kernel.
+// ---------------------------------------------------------------------------------------------
+template <class SH>
+struct BwdLayout2 {
+    static constexpr int C = SH::C, N = SH::N, P = SH::P;
+    // ... and a state small enough for two copies in registers (c2's (8,5,3): 2 x 82 floats; c4's
+    // (4,7,4) with 2 x 106 spills and runs 16% slower than the one-prefix kernel)
+    static constexpr bool OK = (C % 2 == 0) && (32 % C == 0) && ((C & (C - 1)) == 0) && P >= 2 &&
+                               ((SH::CP / 2) % 32 == 0) && 2 * (SH::OWN + SH::OWNA) <= 176;
+    static constexpr int NT = SH::CP / 2;
+    static constexpr int HW = NT / 32;
+    __host__ __device__ static int tile(int64_t M) {
+        int T = 128;
+        while (T > 1 && (size_t)T * HW * C * sizeof(float) > 96 * 1024) T >>= 1;
+        return (int)(T < M ? T : M);
+    }
+    static size_t smem_bytes(int64_t M) {
+        const size_t zf = (size_t)((M * C + 3) / 4 * 4);
+        const size_t T = (size_t)tile(M);
+        return (zf + T * HW * C + T * C + 32) * sizeof(float);
+    }
+};
+
+// the prefix chain of chain K up to level J (J <= P-1): Bp[j] = B^(K)_j[p[:j]], j = 1..J (Bp[0] = 1)
+template <class SH, int K, int J>
+__device__ __forceinline__ void chain_low(float (&Bp)[SH::PL1], const float (&low)[SH::LOWA], const float (&zp)[SH::PD]) {
+    Bp[0] = 1.0f;
+    static_for<1, J + 1>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        if constexpr (j == 1) Bp[j] = fmaf(zp[0], inv_int(K), low[j]);
+        else Bp[j] = fmaf(Bp[j - 1] * inv_int(K - j + 1), zp[j - 1], low[j]);
+    });
+}
+
+// reversal A <- A [x] exp(-z) on levels < N for both prefixes (fused_mulexp with NEG, split at P)
+template <class SH>
+__device__ __forceinline__ void reverse2(float (&Aa)[SH::OWNA], float (&Ab)[SH::OWNA], float (&low)[SH::LOWA],
+                                         const float (&z)[SH::C], const float (&zp)[SH::PD], float zpb) {
+    constexpr int P = SH::P, N = SH::N;
+    static_for<0, N - 1 - P + 1>([&](auto kkc) {
+        constexpr int k = N - 1 - decltype(kkc)::value;  // N-1 .. P
+        // shared part of the chain: levels 1..P-1, then level P per prefix
+        float b = 1.0f;
+        static_for<1, P>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if constexpr (i == 1) b = fmaf(zp[0], -inv_int(k), low[i]);
+            else b = fmaf(b * (-inv_int(k - i + 1)), zp[i - 1], low[i]);
+        });
+        const float bs = b * (-inv_int(k - P + 1));
+        const float ba = fmaf(bs, zp[P - 1], Aa[SH::own_off(P)]);
+        const float bb = fmaf(bs, zpb, Ab[SH::own_off(P)]);
+        if constexpr (k == P) {
+            Aa[SH::own_off(P)] = ba;
+            Ab[SH::own_off(P)] = bb;
+        } else {
+            horner_visit<SH, k, P, 0, true>(ba, Aa, z);
+            horner_visit<SH, k, P, 0, true>(bb, Ab, z);
+        }
+    });
+    static_for<0, P - 1>([&](auto kkc) {
+        constexpr int k = P - 1 - decltype(kkc)::value;
+        float b = 1.0f;
+        static_for<1, k + 1>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if constexpr (i == 1) b = fmaf(zp[0], -inv_int(k), low[i]);
+            else b = fmaf(b * (-inv_int(k - i + 1)), zp[i - 1], low[i]);
+        });
+        low[k] = b;
+    });
+}
+
+template <class SH>
+__global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const BwdParams prm) {
+    using LY = BwdLayout2<SH>;
+    constexpr int C = SH::C, N = SH::N, P = SH::P;
+    constexpr int HW = LY::HW;
+    extern __shared__ __align__(16) float sm[];
+    const int64_t bidx = blockIdx.x;
+    const int64_t M = prm.M;
+    const int T = LY::tile(M);
+    float* zbuf = sm;                                 // [M][C] increments
+    float* part = zbuf + (M * C + 3) / 4 * 4;         // [T][HW][C] per-warp gz records
+    float* tot = part + (size_t)T * HW * C;           // [T][C] per-step gz totals
+    float* gprev = tot + (size_t)T * C;               // [C]
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int has_bp = prm.bp_mode != 0;
+    const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;
+    const float* gorow = prm.grad_out + (size_t)bidx * prm.go_stride;
+
+    for (int64_t e = tid; e < M * C; e += blockDim.x) {
+        const int64_t s = e / C;
+        const int c = (int)(e % C);
+        const float* xr = prm.path + bidx * prm.L * C;
+        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
+        const float x1 = xr[r1 * C + c];
+        const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
+        zbuf[e] = prm.zsign * (x1 - x0);
+    }
+    if (tid < C) gprev[tid] = 0.0f;
+
+    const int pa = 2 * tid;  // prefixes pa, pa + 1 (siblings: same p[:P-1], last digit p[P-1], p[P-1] + 1)
+    int p[SH::PD];
+    prefix_digits<SH>(pa, p);
+    float Aa[SH::OWNA], Ab[SH::OWNA], Ga[SH::OWN], Gb[SH::OWN];
+    float low[SH::LOWA], Gh[SH::LOWA];
+    static_for<SH::K0, N>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        load_run<SH::own(k), SH::own_off(k)>(Aa, sigrow + SH::lvl_off(k) + (int64_t)pa * SH::own(k));
+        load_run<SH::own(k), SH::own_off(k)>(Ab, sigrow + SH::lvl_off(k) + (int64_t)(pa + 1) * SH::own(k));
+    });
+    static_for<SH::K0, N + 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        load_run<SH::own(k), SH::own_off(k)>(Ga, gorow + SH::lvl_off(k) + (int64_t)pa * SH::own(k));
+        load_run<SH::own(k), SH::own_off(k)>(Gb, gorow + SH::lvl_off(k) + (int64_t)(pa + 1) * SH::own(k));
+    });
+    low[0] = 0.0f;
+    Gh[0] = 0.0f;
+    static_for<1, P>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        constexpr int tail = (int)ipow(C, P - i);
+        low[i] = sigrow[SH::lvl_off(i) + pa / tail];
+        Gh[i] = (pa % tail == 0) ? gorow[SH::lvl_off(i) + pa / tail] : 0.0f;
+    });
+    __syncthreads();
+    if (SIG_BWD2_STAGGER > 0 && ((warp >> 2) & 1)) __nanosleep(SIG_BWD2_STAGGER);
+
+    // channels of the level-P (pa, pb) and level-(P-1) partials in the reduction (see below)
+    constexpr int HC = C / 2;
+    const int gbase = lane & ~(C - 1);
+    const int ch = lane & (C - 1);
+    const int chP1 = (tid / HC) % C;                        // p_{P-2} of this thread
+    const int chP1_g0 = ((tid & ~(C - 1)) / HC) % C;        // ... of sub-group 0 of its C-lane group
+    const int chP1_g1 = (((tid & ~(C - 1)) + HC) / HC) % C; // ... of sub-group 1
+    (void)chP1;
+
+    for (int64_t n0 = 0; n0 < M; n0 += T) {
+        const int tn = (int)((M - n0) < T ? (M - n0) : T);
+        for (int j = 0; j < tn; ++j) {
+            const int64_t t = M - 1 - (n0 + j);
+            float z[C], zp[SH::PD];
+#pragma unroll
+            for (int c = 0; c < C; ++c) z[c] = zbuf[t * C + c];
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zp[q] = zbuf[t * C + p[q]];
+            const float zpb = zbuf[t * C + p[P - 1] + 1];
+            // (1) reversibility: levels < N; the exact start state (identity) at t = 0
+            if (t > 0) {
+                reverse2<SH>(Aa, Ab, low, z, zp, zpb);
+            } else {
+#pragma unroll
+                for (int q = 0; q < SH::OWNA; ++q) Aa[q] = Ab[q] = 0.0f;
+#pragma unroll
+                for (int q = 0; q < SH::LOWA; ++q) low[q] = 0.0f;
+            }
+            // (2)+(3): chains k = 1..N bottom-up
+            float gz[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) gz[c] = 0.0f;
+            float acc[SH::PL1];
+#pragma unroll
+            for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
+            float accPb = 0.0f;  // level-P partial of pb (acc[P] is pa's)
+            static_for<1, P>([&](auto kc) {  // chains entirely below P
+                constexpr int k = decltype(kc)::value;
+                float Bp[SH::PL1];
+                chain_low<SH, k, k - 1>(Bp, low, zp);
+                low_tail<SH, k, k>(Gh[k], Bp, zp, acc, Gh);
+            });
+            static_for<P, N + 1>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                constexpr float sc = inv_int(k - P + 1);
+                float Bp[SH::PL1];
+                chain_low<SH, k, P - 1>(Bp, low, zp);
+                float ba, bb;
+                if constexpr (k == P) {
+                    ba = Ga[SH::own_off(P)];
+                    bb = Gb[SH::own_off(P)];
+                } else {
+                    const float bs = Bp[P - 1] * sc;
+                    ba = vjp_visit<SH, k, P, 0>(fmaf(bs, zp[P - 1], Aa[SH::own_off(P)]), Ga, Aa, z, gz);
+                    bb = vjp_visit<SH, k, P, 0>(fmaf(bs, zpb, Ab[SH::own_off(P)]), Gb, Ab, z, gz);
+                }
+                // level P of the low tail per prefix, then one shared tail from level P-1
+                const float bps = Bp[P - 1] * sc;
+                acc[P] = fmaf(bps, ba, acc[P]);
+                accPb = fmaf(bps, bb, accPb);
+                const float b1 = fmaf(ba * zp[P - 1], sc, (bb * zpb) * sc);
+                Gh[P - 1] += b1;
+                low_tail<SH, k, P - 1>(b1, Bp, zp, acc, Gh);
+            });
+
+            // ---- per-step gz: warp reduction into the tile
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = gz[c];
+            static_for<0, ilog2(C)>([&](auto sc_) {
+                constexpr int m = C >> (decltype(sc_)::value + 1);
+                const bool up = (lane & m) != 0;
+#pragma unroll
+                for (int q = 0; q < m; ++q) {
+                    const float send = up ? v[q] : v[q + m];
+                    const float keep = up ? v[q + m] : v[q];
+                    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                }
+            });
+            float tv = v[0];  // channel ch = lane % C, summed over the C-lane group
+            {
+                // level P: pa -> channel 2 (tid % HC), pb -> +1; lanes j and j + HC of a group share them
+                const float u0 = acc[P] + __shfl_xor_sync(0xffffffffu, acc[P], HC);
+                const float u1 = accPb + __shfl_xor_sync(0xffffffffu, accPb, HC);
+                const float t0 = __shfl_sync(0xffffffffu, u0, gbase + (ch >> 1));
+                const float t1 = __shfl_sync(0xffffffffu, u1, gbase + (ch >> 1));
+                tv += (ch & 1) ? t1 : t0;
+            }
+            {
+                // level P-1: channel p_{P-2}, constant over each half (HC lanes) of the group
+                float gs = acc[P - 1];
+#pragma unroll
+                for (int m = 1; m < HC; m <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, m);
+                const float s0 = __shfl_sync(0xffffffffu, gs, gbase);
+                const float s1 = __shfl_sync(0xffffffffu, gs, gbase + HC);
+                if (ch == chP1_g0) tv += s0;
+                if (ch == chP1_g1) tv += s1;
+            }
+            static_for<1, P - 1>([&](auto ic) {  // levels below P-1: channel constant over the group
+                constexpr int i = decltype(ic)::value;
+                float gsum = acc[i];
+#pragma unroll
+                for (int m = 1; m < C; m <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, m);
+                if (ch == p[i - 1]) tv += gsum;
+            });
+#pragma unroll
+            for (int m = C; m < 32; m <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, m);
+            if (lane < C) part[((size_t)j * HW + warp) * C + lane] = tv;
+        }
+        // ---- flush
+        __syncthreads();
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            float s = 0.0f;
+            for (int w = 0; w < HW; ++w) s += part[((size_t)j * HW + w) * C + c];
+            tot[j * C + c] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            const int64_t t = M - 1 - (n0 + j);
+            const float before = (j == 0) ? gprev[c] : tot[(j - 1) * C + c];
+            const int64_t r = t + 1;  // augmented point t + 1
+            float* gr = has_bp ? prm.grad_path + (bidx * prm.L + (r - 1)) * C : prm.grad_path + (bidx * prm.L + r) * C;
+            gr[c] = prm.zsign * (tot[j * C + c] - before);
+            if (t == 0) {
+                float* g0 = has_bp ? ((prm.bp_mode == 2 && prm.grad_bp) ? prm.grad_bp + bidx * C : nullptr)
+                                   : prm.grad_path + bidx * prm.L * C;
+                if (g0) g0[c] = -prm.zsign * tot[j * C + c];
+            }
+        }
+        __syncthreads();
+        if (tid < C) gprev[tid] = tot[(tn - 1) * C + tid];
+        __syncthreads();
+    }
+}
+
+#ifndef SIG_BWD2
+#define SIG_BWD2 1
+#endif
+
 template <class SH>
 cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
+    if constexpr (SIG_BWD2 && BwdLayout2<SH>::OK) {
+        using LY2 = BwdLayout2<SH>;
+        if (!prm.stream && prm.n_chunks == 1 && prm.initial == nullptr && prm.grad_initial == nullptr) {
+            const size_t smem2 = LY2::smem_bytes(prm.M);
+            if (smem2 <= 227 * 1024) {
+                if (smem2 > 48 * 1024) {
+                    cudaError_t e = cudaFuncSetAttribute(sig_bwd2_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem2);
+                    if (e != cudaSuccess) return e;
+                }
+                sig_bwd2_kernel<SH><<<(unsigned)prm.B, LY2::NT, smem2, st>>>(prm);
+                return cudaGetLastError();
+            }
+        }
+    }
     using LY = BwdLayout<SH>;
     const size_t smem = LY::smem_bytes(prm.chunk_len);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
