@@ -521,7 +521,7 @@ struct BwdLayout2 {
     // ... and a state small enough for two copies in registers (c2's (8,5,3): 2 x 82 floats; c4's
     // (4,7,4) with 2 x 106 spills and runs 16% slower than the one-prefix kernel)
     static constexpr bool OK = (C % 2 == 0) && (32 % C == 0) && ((C & (C - 1)) == 0) && P >= 2 &&
-                               ((SH::CP / 2) % 32 == 0) && 2 * (SH::OWN + SH::OWNA) <= 176;
+                               ((SH::CP / 2) % 32 == 0) && SH::CP / 2 <= 512 && 2 * (SH::OWN + SH::OWNA) <= 176;
     static constexpr int NT = SH::CP / 2;
     static constexpr int HW = NT / 32;
     __host__ __device__ static int tile(int64_t M) {
@@ -544,43 +544,6 @@ __device__ __forceinline__ void chain_low(float (&Bp)[SH::PL1], const float (&lo
         constexpr int j = decltype(jc)::value;
         if constexpr (j == 1) Bp[j] = fmaf(zp[0], inv_int(K), low[j]);
         else Bp[j] = fmaf(Bp[j - 1] * inv_int(K - j + 1), zp[j - 1], low[j]);
-    });
-}
-
-// reversal A <- A [x] exp(-z) on levels < N for both prefixes (fused_mulexp with NEG, split at P)
-template <class SH>
-__device__ __forceinline__ void reverse2(float (&Aa)[SH::OWNA], float (&Ab)[SH::OWNA], float (&low)[SH::LOWA],
-                                         const float (&z)[SH::C], const float (&zp)[SH::PD], float zpb) {
-    constexpr int P = SH::P, N = SH::N;
-    static_for<0, N - 1 - P + 1>([&](auto kkc) {
-        constexpr int k = N - 1 - decltype(kkc)::value;  // N-1 .. P
-        // shared part of the chain: levels 1..P-1, then level P per prefix
-        float b = 1.0f;
-        static_for<1, P>([&](auto ic) {
-            constexpr int i = decltype(ic)::value;
-            if constexpr (i == 1) b = fmaf(zp[0], -inv_int(k), low[i]);
-            else b = fmaf(b * (-inv_int(k - i + 1)), zp[i - 1], low[i]);
-        });
-        const float bs = b * (-inv_int(k - P + 1));
-        const float ba = fmaf(bs, zp[P - 1], Aa[SH::own_off(P)]);
-        const float bb = fmaf(bs, zpb, Ab[SH::own_off(P)]);
-        if constexpr (k == P) {
-            Aa[SH::own_off(P)] = ba;
-            Ab[SH::own_off(P)] = bb;
-        } else {
-            horner_visit<SH, k, P, 0, true>(ba, Aa, z);
-            horner_visit<SH, k, P, 0, true>(bb, Ab, z);
-        }
-    });
-    static_for<0, P - 1>([&](auto kkc) {
-        constexpr int k = P - 1 - decltype(kkc)::value;
-        float b = 1.0f;
-        static_for<1, k + 1>([&](auto ic) {
-            constexpr int i = decltype(ic)::value;
-            if constexpr (i == 1) b = fmaf(zp[0], -inv_int(k), low[i]);
-            else b = fmaf(b * (-inv_int(k - i + 1)), zp[i - 1], low[i]);
-        });
-        low[k] = b;
     });
 }
 
@@ -662,7 +625,7 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const B
             const float zpb = zbuf[t * C + p[P - 1] + 1];
             // (1) reversibility: levels < N; the exact start state (identity) at t = 0
             if (t > 0) {
-                reverse2<SH>(Aa, Ab, low, z, zp, zpb);
+                mulexp2<SH, N - 1, true>(Aa, Ab, low, z, zp, zpb);
             } else {
 #pragma unroll
                 for (int q = 0; q < SH::OWNA; ++q) Aa[q] = Ab[q] = 0.0f;

@@ -126,6 +126,46 @@ __device__ __forceinline__ void fused_mulexp(float (&own)[SZ], float (&low)[SH::
     });
 }
 
+// A <- A [x] exp(+-z) for two sibling prefixes pa, pb = pa + 1 held by one thread (same p[:P-1]; the
+// last letters are p[P-1] and p[P-1] + 1, zpb = z[p[P-1] + 1]): the prefix chain below level P and
+// the replicated low levels are computed once, level P and above per prefix (the two-prefix
+// kernels sig_fwd2_kernel / sig_bwd2_kernel; P >= 2).
+template <class SH, int KTOP, bool NEG, int SZ>
+__device__ __forceinline__ void mulexp2(float (&Aa)[SZ], float (&Ab)[SZ], float (&low)[SH::LOWA], const float (&z)[SH::C],
+                                        const float (&zp)[SH::PD], float zpb) {
+    constexpr int P = SH::P;
+    constexpr float sg = NEG ? -1.0f : 1.0f;
+    static_for<0, KTOP - P + 1>([&](auto kkc) {
+        constexpr int k = KTOP - decltype(kkc)::value;  // KTOP .. P
+        float b = 1.0f;
+        static_for<1, P>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if constexpr (i == 1) b = fmaf(zp[0], sg * inv_int(k), low[i]);
+            else b = fmaf(b * (sg * inv_int(k - i + 1)), zp[i - 1], low[i]);
+        });
+        const float bs = b * (sg * inv_int(k - P + 1));
+        const float ba = fmaf(bs, zp[P - 1], Aa[SH::own_off(P)]);
+        const float bb = fmaf(bs, zpb, Ab[SH::own_off(P)]);
+        if constexpr (k == P) {
+            Aa[SH::own_off(P)] = ba;
+            Ab[SH::own_off(P)] = bb;
+        } else {
+            horner_visit<SH, k, P, 0, NEG>(ba, Aa, z);
+            horner_visit<SH, k, P, 0, NEG>(bb, Ab, z);
+        }
+    });
+    static_for<0, P - 1>([&](auto kkc) {
+        constexpr int k = P - 1 - decltype(kkc)::value;
+        float b = 1.0f;
+        static_for<1, k + 1>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if constexpr (i == 1) b = fmaf(zp[0], sg * inv_int(k), low[i]);
+            else b = fmaf(b * (sg * inv_int(k - i + 1)), zp[i - 1], low[i]);
+        });
+        low[k] = b;
+    });
+}
+
 // Write the thread's coefficients of the current state to a row of S floats.
 template <class SH, bool STREAMING>
 __device__ __forceinline__ void store_state(float* row, int prefix, const float (&own)[SH::OWN],
@@ -431,8 +471,79 @@ cudaError_t launch_fwd_stream_staged(const FwdParams& prm_in, cudaStream_t st, b
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Forward with two sibling prefixes per thread (cf. sig_bwd2_kernel): one path per CTA of CP/2
+// threads; the prefix chains below level P and the replicated low levels are computed once for both
+// prefixes.  Plain calls only (no stream, no time chunks, no initial state).
+// ---------------------------------------------------------------------------------------------
+template <class SH>
+struct FwdLayout2 {
+    static constexpr bool OK = (SH::C % 2 == 0) && SH::P >= 2 && ((SH::CP / 2) % 32 == 0) && SH::CP / 2 <= 512 &&
+                               2 * SH::OWN <= 160;
+    static constexpr int NT = SH::CP / 2;
+};
+
+template <class SH>
+__global__ void __launch_bounds__(FwdLayout2<SH>::NT, 1) sig_fwd2_kernel(const FwdParams prm) {
+    constexpr int C = SH::C, P = SH::P;
+    extern __shared__ __align__(16) float zs[];  // [T][C]
+    const int64_t b = blockIdx.x;
+    const int64_t M = prm.M;
+    const int T = prm.tile;
+    const int has_bp = prm.bp_mode != 0;
+    const int pa = 2 * threadIdx.x;
+    int p[SH::PD];
+    prefix_digits<SH>(pa, p);
+    float Aa[SH::OWN], Ab[SH::OWN], low[SH::LOWA];
+#pragma unroll
+    for (int i = 0; i < SH::OWN; ++i) Aa[i] = Ab[i] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < SH::LOWA; ++i) low[i] = 0.0f;
+    for (int64_t t0 = 0; t0 < M; t0 += T) {
+        __syncthreads();
+        const int tl = (int)(M - t0 < T ? M - t0 : T);
+        const int64_t rowbase = (b * prm.L + (t0 - has_bp)) * C;
+        for (int i = threadIdx.x; i < tl * C; i += blockDim.x) {
+            const int c = i % C;
+            const int64_t g = rowbase + i;
+            const float x1 = __ldg(prm.path + g + C);
+            float x0;
+            if (g >= b * prm.L * C) x0 = __ldg(prm.path + g);
+            else x0 = (prm.bp_mode == 2) ? prm.basepoint[b * C + c] : 0.0f;
+            zs[i] = prm.zsign * (x1 - x0);
+        }
+        __syncthreads();
+        for (int t = 0; t < tl; ++t) {
+            float z[C], zp[SH::PD];
+#pragma unroll
+            for (int c = 0; c < C; ++c) z[c] = zs[t * C + c];
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zp[q] = zs[t * C + p[q]];
+            const float zpb = zs[t * C + p[P - 1] + 1];
+            mulexp2<SH, SH::N, false>(Aa, Ab, low, z, zp, zpb);
+        }
+    }
+    float* row = prm.out + (size_t)b * SH::S;
+    store_state<SH, false>(row, pa, Aa, low);
+    store_state<SH, false>(row, pa + 1, Ab, low);  // pa + 1 is odd: writes no replicated level
+}
+
+#ifndef SIG_FWD2
+#define SIG_FWD2 1
+#endif
+
 template <class SH>
 cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
+    if constexpr (SIG_FWD2 && FwdLayout2<SH>::OK) {
+        if (!prm_in.stream && prm_in.n_chunks == 1 && prm_in.upc == 0 && prm_in.initial == nullptr &&
+            prm_in.B >= 148) {
+            FwdParams prm = prm_in;
+            prm.tile = (int)(prm.M < 256 ? prm.M : 256);
+            const size_t smem = (size_t)prm.tile * SH::C * sizeof(float);
+            sig_fwd2_kernel<SH><<<(unsigned)prm.B, FwdLayout2<SH>::NT, smem, st>>>(prm);
+            return cudaGetLastError();
+        }
+    }
 #if !defined(SIG_STREAM_DIRECT)
     {
         bool done = false;
