@@ -190,3 +190,27 @@ def test_c3_full_size_sampled():
     err = level_rel_err(got, ref, C, N)
     print(f"PARITY c3 full-size sampled: {err:.3e}")
     assert err < FWD_TOL
+
+
+@pytest.mark.parametrize("C,N", [(8, 4), (8, 5)])
+@pytest.mark.parametrize("bp", [None, "zero", "given"])
+def test_two_prefix_kernels(C, N, bp):
+    """Shapes and batch sizes that take the two-prefix kernels (sig_fwd2_kernel: B >= 148;
+    sig_bwd2_kernel), with every basepoint mode; every 16th path checked against the oracle."""
+    B, L = 150, 23
+    x = brownian_paths(B, L, C, seed=40 + N)
+    S = sum(C ** k for k in range(1, N + 1))
+    g = normal((B, S), seed=41 + N)
+    bpa = normal((B, C), seed=42, scale=0.3) if bp == "given" else None
+    xt = _cuda(x).requires_grad_(True)
+    bpt = _cuda(bpa).requires_grad_(True) if bp == "given" else (True if bp == "zero" else None)
+    out = sb.signature(xt, N, basepoint=bpt)
+    out.backward(_cuda(g))
+    idx = np.arange(0, B, 16)
+    obp = bpa[idx] if bp == "given" else (True if bp == "zero" else None)
+    ref = oracle.signature(x[idx], N, basepoint=obp, threads=8)
+    assert level_rel_err(out.detach().cpu().numpy()[idx], ref, C, N) < FWD_TOL
+    rx, rb = oracle.signature_vjp(g[idx], x[idx], N, basepoint=obp, threads=8)
+    assert path_rel_err(xt.grad.cpu().numpy()[idx], rx) < BWD_TOL
+    if bp == "given":
+        assert path_rel_err(bpt.grad.cpu().numpy()[idx], rb) < BWD_TOL
