@@ -518,11 +518,13 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
 template <class SH>
 struct BwdLayout2 {
     static constexpr int C = SH::C, N = SH::N, P = SH::P;
-    // ... and a state small enough for two copies in registers (c2's (8,5,3): 2 x 82 floats; c4's
-    // (4,7,4) with 2 x 106 spills and runs 16% slower than the one-prefix kernel)
-    static constexpr bool OK = (C % 2 == 0) && (32 % C == 0) && ((C & (C - 1)) == 0) && P >= 2 &&
-                               ((SH::CP / 2) % 32 == 0) && SH::CP / 2 <= 512 && 2 * (SH::OWN + SH::OWNA) <= 176;
+    // ... and a state small enough for two copies plus ~60 working registers in the per-thread share
+    // of the register file (c2's (8,5,3): 2 x 82 floats; c4's (4,7,4) with 2 x 106 spills and ran
+    // 16% slower than the one-prefix kernel)
     static constexpr int NT = SH::CP / 2;
+    static constexpr int REGS = (65536 / (NT > 0 ? NT : 1)) < 255 ? (65536 / (NT > 0 ? NT : 1)) : 255;
+    static constexpr bool OK = (C % 2 == 0) && (32 % C == 0) && ((C & (C - 1)) == 0) && P >= 2 && (NT % 32 == 0) &&
+                               NT <= 512 && 2 * (SH::OWN + SH::OWNA) + 48 + 4 * P <= REGS;
     static constexpr int HW = NT / 32;
     __host__ __device__ static int tile(int64_t M) {
         int T = 128;

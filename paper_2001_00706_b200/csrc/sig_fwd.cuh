@@ -478,9 +478,12 @@ cudaError_t launch_fwd_stream_staged(const FwdParams& prm_in, cudaStream_t st, b
 // ---------------------------------------------------------------------------------------------
 template <class SH>
 struct FwdLayout2 {
-    static constexpr bool OK = (SH::C % 2 == 0) && SH::P >= 2 && ((SH::CP / 2) % 32 == 0) && SH::CP / 2 <= 512 &&
-                               2 * SH::OWN <= 160;
     static constexpr int NT = SH::CP / 2;
+    // both prefixes' state plus ~48 working registers must fit the per-thread share of the register
+    // file (c2's (8,5,3): 2 x 73 at 256 threads; c4's (4,7,4): 2 x 85 at 128 threads)
+    static constexpr int REGS = (65536 / (NT > 0 ? NT : 1)) < 255 ? (65536 / (NT > 0 ? NT : 1)) : 255;
+    static constexpr bool OK = (SH::C % 2 == 0) && SH::P >= 2 && (NT % 32 == 0) && NT <= 512 &&
+                               2 * SH::OWN + 48 <= REGS;
 };
 
 template <class SH>
