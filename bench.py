@@ -330,7 +330,7 @@ class Workload:
             f_fwd = alg_flops("fwd", B, M, C, N)
             f_bwd = alg_flops("bwd", B, M, C, N)
             ach = f_bwd / (seg_ms["bwd"] / 1000) / 1e12
-            kern = ("sig_bwd_kernel (reversible backward)" if op == "sig_fwd_bwd"
+            kern = ("sig_bwd2_kernel (reversible backward, two prefixes per thread)" if op == "sig_fwd_bwd"
                     else "sig_logsignature_backward call = logsig_bwd_kernel + sig_bwd_kernel (sig-bwd FLOPs only)")
             return {"bound": "alu", "kernel": kern, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                     "frac": ach / peak, "traffic": traffic.get("sig_bwd_kernel"), "peak_source": peak_src,

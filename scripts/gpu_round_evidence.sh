@@ -10,9 +10,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --steps 8 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv \
     python bench.py --config c4 --steps 8 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sig_bwd_kernel -s 1 -c 1 -o gpurun_out/c2_k2_full \
+ncu --set full --clock-control none --import-source on -k regex:sig_bwd2_kernel -s 1 -c 1 -o gpurun_out/c2_k2_full \
     python scripts/profile_c2.py c2 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sig_fwd_kernel -s 1 -c 1 -o gpurun_out/c2_k1_full \
+ncu --set full --clock-control none --import-source on -k regex:sig_fwd2_kernel -s 1 -c 1 -o gpurun_out/c2_k1_full \
     python scripts/profile_c2.py c2 3 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sig_fwd_stream_kernel -s 1 -c 1 -o gpurun_out/c3_stream_full \
     python scripts/profile_c2.py c3 3 > /dev/null 2>&1
