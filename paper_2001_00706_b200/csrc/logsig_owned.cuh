@@ -253,10 +253,18 @@ __global__ void __launch_bounds__(LOGSIG_THREADS, 1) logsig_bwd_owned_t_kernel(c
                 for (int e = p.tb.minvT_rowptr[j]; e < p.tb.minvT_rowptr[j + 1]; ++e)
                     v = fma((double)p.tb.minvT_val[e], (double)go[p.tb.minvT_col[e]], v);
             }
+            // level of f and its padded slot from compile-time tables (a runtime T::off / T::gls
+            // would loop over powers of C for every word: a quarter of the kernel's instructions)
             const int f = (int)p.tb.lyn_idx[j];
-            int k = 1;
-            while (k < N && f >= T::off(k + 1)) ++k;
-            gl[T::gls(k) + lpad(f - T::off(k))] = (float)v;
+            int base = T::gls(1), offk = 0;
+            static_for<2, N + 1>([&](auto kc) {
+                constexpr int kk = decltype(kc)::value;
+                if (f >= T::off(kk)) {
+                    base = T::gls(kk);
+                    offk = T::off(kk);
+                }
+            });
+            gl[base + lpad(f - offk)] = (float)v;
         }
     }
     __syncthreads();
