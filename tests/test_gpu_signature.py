@@ -235,3 +235,27 @@ def test_host_pipeline_matches_direct():
         pipe.run(fn)
         torch.cuda.synchronize()
         assert torch.equal(out, ref.cpu())
+
+
+def test_c5_full_size():
+    """BASELINE config c5 at full size: one path of L = 2^22 points, C = 3, N = 6, in the launch
+    configuration bench.py times (time chunks folded in order).  The float64 oracle is run on 64
+    time chunks in parallel (chunk j = points [j m, (j+1) m], sharing boundary points) and folded
+    with its own [x] in time order -- Chen's identity, pinned by the oracle tests."""
+    C, N, L = 3, 6, 2 ** 22
+    x = brownian_paths(1, L, C, seed=5)
+    got = sb.sig_signature(_cuda(x), N).cpu().numpy()
+    nch = 64
+    M = L - 1
+    edges = [round(j * M / nch) for j in range(nch + 1)]
+    m = max(b - a for a, b in zip(edges, edges[1:]))
+    chunks = np.zeros((nch, m + 1, C), np.float32)
+    for j, (a, b) in enumerate(zip(edges, edges[1:])):
+        seg = x[0, a:b + 1]
+        chunks[j, :len(seg)] = seg
+        chunks[j, len(seg):] = seg[-1]  # repeated end point: a zero increment changes nothing
+    sigs = oracle.signature(chunks, N, threads=16)
+    ref = oracle.multi_combine(sigs[:, None, :], C, N)
+    err = level_rel_err(got, ref.reshape(1, -1), C, N)
+    print(f"PARITY c5 full-size: {err:.3e}")
+    assert err < FWD_TOL
