@@ -26,6 +26,8 @@
 //   channel into a shared-memory tile; every T steps the CTA sums the tile in a fixed order and
 //   writes the gradient rows.  No cross-warp synchronisation inside a tile.
 // All reductions have a fixed order, so results are bitwise reproducible.
+// sig_bwd2_kernel (below) is the same algorithm with two sibling prefixes per thread, chosen for
+// plain calls of shapes whose doubled state fits the register file.
 #pragma once
 #include "sig_fwd.cuh"
 
@@ -610,10 +612,8 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const B
     constexpr int HC = C / 2;
     const int gbase = lane & ~(C - 1);
     const int ch = lane & (C - 1);
-    const int chP1 = (tid / HC) % C;                        // p_{P-2} of this thread
     const int chP1_g0 = ((tid & ~(C - 1)) / HC) % C;        // ... of sub-group 0 of its C-lane group
     const int chP1_g1 = (((tid & ~(C - 1)) + HC) / HC) % C; // ... of sub-group 1
-    (void)chP1;
 
     for (int64_t n0 = 0; n0 < M; n0 += T) {
         const int tn = (int)((M - n0) < T ? (M - n0) : T);
