@@ -192,11 +192,12 @@ def test_c3_full_size_sampled():
     assert err < FWD_TOL
 
 
-@pytest.mark.parametrize("C,N", [(8, 4), (8, 5)])
+@pytest.mark.parametrize("C,N", [(8, 2), (8, 3), (8, 4), (8, 5), (4, 6), (4, 7), (2, 11)])
 @pytest.mark.parametrize("bp", [None, "zero", "given"])
 def test_two_prefix_kernels(C, N, bp):
-    """Shapes and batch sizes that take the two-prefix kernels (sig_fwd2_kernel: B >= 148;
-    sig_bwd2_kernel), with every basepoint mode; every 16th path checked against the oracle."""
+    """Shapes and batch sizes that take the two-prefix kernels (sig_fwd2_kernel: B >= 148, shapes
+    (8,4), (8,5), (4,6), (4,7), (2,11); sig_bwd2_kernel: (8,2)..(8,5)), with every basepoint mode;
+    every 16th path checked against the oracle."""
     B, L = 150, 23
     x = brownian_paths(B, L, C, seed=40 + N)
     S = sum(C ** k for k in range(1, N + 1))
