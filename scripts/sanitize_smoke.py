@@ -1,0 +1,31 @@
+"""Dev: small calls of every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import sys
+import torch
+sys.path.insert(0, ".")
+import paper_2001_00706_b200 as sb
+from synth import brownian_paths, normal
+
+def cu(a):
+    return torch.from_numpy(a).cuda()
+
+# two-prefix forward/backward (C=8, N=4, B >= 148), basepoint given
+x = cu(brownian_paths(150, 9, 8, 1))
+bp = cu(normal((150, 8), 2))
+s = sb.sig_signature(x, 4, basepoint=bp)
+g = cu(normal((150, s.shape[1]), 3))
+sb.sig_signature_backward(g, x, s, 4, basepoint=bp)
+# one-prefix kernels, stream mode (staged TMA rows, odd S, several paths per CTA)
+x2 = cu(brownian_paths(400, 13, 5, 4))
+st = sb.sig_signature(x2, 3, stream=True)
+sb.sig_signature_backward(cu(normal(tuple(st.shape), 5)), x2, st, 3, stream=True)
+# time-chunked long path, forward and backward
+x3 = cu(brownian_paths(1, 5000, 3, 6))
+s3 = sb.sig_signature(x3, 4)
+sb.sig_signature_backward(cu(normal((1, s3.shape[1]), 7)), x3, s3, 4)
+# logsignature (compiled K4/K5) words and brackets
+x4 = cu(brownian_paths(3, 20, 4, 8))
+for mode in ("words", "brackets", "expand"):
+    o, sg = sb.sig_logsignature(x4, 5, mode, return_signature=True)
+    sb.sig_logsignature_backward(cu(normal(tuple(o.shape), 9)), x4, sg, 5, mode)
+torch.cuda.synchronize()
+print("ok")
