@@ -110,6 +110,26 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
                                     const float* basepoint, float* grad_path, float* grad_basepoint,
                                     sig_cuda_stream_t s);
 
+/* ---------------------------------------------------------------- host-resident batches */
+
+/* Signature forward + reversible backward of a batch that lives in HOST memory (the training step
+ * of BASELINE config c2 fed from the host): the batch is cut into `chunks` slices; per slice the
+ * host->device copies of path and grad_out run on an internal copy stream, the forward and
+ * backward kernels (sig_signature, sig_signature_backward) on `s` once the slice has arrived, and
+ * the device->host copy of its grad_path on a second internal stream -- so copies of one slice
+ * overlap the kernels of another.  Work on `s` issued before the call is ordered before the copies,
+ * and `s` waits for the last read-back, so the host results are valid once `s` completes.
+ *   path_h       [B, L, C] host, read   (pinned memory for the copies to overlap)
+ *   grad_out_h   [B, S] host, read      (the upstream gradient of the final signature)
+ *   grad_path_h  [B, L, C] host, written
+ *   ws           device workspace of sig_signature_fwd_bwd_host_workspace_size(...) bytes (holds the
+ *                device copies of the inputs, the signatures, the gradients; caller-owned)
+ * No basepoint, no stream mode.  Returns the first failing call's status. */
+size_t sig_signature_fwd_bwd_host_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t chunks);
+sig_status_t sig_signature_fwd_bwd_host(const float* path_h, const float* grad_out_h, int64_t B, int64_t L, int64_t C,
+                                        int32_t depth, float* grad_path_h, int32_t chunks, void* ws, size_t ws_bytes,
+                                        sig_cuda_stream_t s);
+
 /* ---------------------------------------------------------------- signature options */
 
 /* The `inverse` and `initial` options (reading R18).

@@ -78,6 +78,9 @@ def lib():
                 ("sig_signature_backward_ex", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32,
                                                              ctypes.c_int, _vp, _c_i32, _vp, _vp, _vp, _vp, _vp,
                                                              _c_sz, _vp]),
+                ("sig_signature_fwd_bwd_host_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32]),
+                ("sig_signature_fwd_bwd_host", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp, _c_i32,
+                                                              _vp, _c_sz, _vp]),
                 ("sig_signature_combine", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _vp]),
                 ("sig_signature_combine_backward", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _vp,
                                                                   _vp]),
@@ -215,6 +218,28 @@ def sig_signature_backward_ex(grad_out, path, out_saved, depth: int, stream: boo
                                          bpm, _ptr(bp), int(inverse), _ptr(ini), _ptr(gp), _ptr(gbp), _ptr(gi),
                                          _ptr(ws), wsb, _stream(path.device)), "sig_signature_backward_ex")
     return gp, gbp, gi
+
+
+def sig_signature_fwd_bwd_host(path_h, grad_out_h, depth: int, chunks: int = 4, grad_path_h=None, device=None):
+    """sig_signature_fwd_bwd_host: forward + reversible backward of a HOST-resident batch, in
+    `chunks` slices whose copies overlap the kernels (include/sig.h).  path_h [B, L, C] and
+    grad_out_h [B, S] are float32 CPU tensors (pinned for the overlap); returns grad_path [B, L, C]
+    in host memory (grad_path_h if given), valid once the current CUDA stream completes."""
+    for name, t in (("path_h", path_h), ("grad_out_h", grad_out_h)):
+        if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous():
+            raise SigError(f"{name} must be a contiguous float32 CPU tensor")
+    B, L, C = path_h.shape
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    Lib = lib()
+    S = Lib.sig_signature_channels(C, depth)
+    if tuple(grad_out_h.shape) != (B, S):
+        raise SigError(f"grad_out_h must be [{B}, {S}]")
+    out = grad_path_h if grad_path_h is not None else torch.empty((B, L, C), dtype=torch.float32).pin_memory()
+    wsb = Lib.sig_signature_fwd_bwd_host_workspace_size(B, L, C, depth, chunks)
+    ws = torch.empty(max(wsb, 1), device=dev, dtype=torch.uint8)
+    _check(Lib.sig_signature_fwd_bwd_host(_ptr(path_h), _ptr(grad_out_h), B, L, C, depth, _ptr(out), chunks,
+                                          _ptr(ws), wsb, _stream(dev)), "sig_signature_fwd_bwd_host")
+    return out
 
 
 def sig_signature_combine(a, b, C: int, depth: int):

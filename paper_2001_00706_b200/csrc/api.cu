@@ -743,6 +743,96 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
                                      grad_path, grad_basepoint, nullptr, nullptr, 0, s);
 }
 
+// ---------------------------------------------------------------- host-resident batches
+// Workspace layout: [path B*L*C][grad_out B*S][sig B*S][grad_path B*L*C][forward workspace of one
+// slice], each region 256-byte aligned.
+static size_t host_fb_layout(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t chunks, size_t off[5]) {
+    const int64_t S = sig_channels_checked(C, depth);
+    if (S < 0 || B < 1 || L < 2 || C < 1 || chunks < 1) return 0;
+    const int64_t bc = (B + chunks - 1) / chunks;
+    size_t o = 0;
+    off[0] = o; o = align256(o + (size_t)B * L * C * sizeof(float));
+    off[1] = o; o = align256(o + (size_t)B * S * sizeof(float));
+    off[2] = o; o = align256(o + (size_t)B * S * sizeof(float));
+    off[3] = o; o = align256(o + (size_t)B * L * C * sizeof(float));
+    off[4] = o;
+    FwdPlan pl;
+    if (make_fwd_plan(bc, L, C, depth, 0, SIG_BP_NONE, pl) != SIG_OK) return 0;
+    return o + align256(pl.ws_bytes);
+}
+
+size_t sig_signature_fwd_bwd_host_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t chunks) {
+    size_t off[5];
+    return host_fb_layout(B, L, C, depth, chunks, off);
+}
+
+sig_status_t sig_signature_fwd_bwd_host(const float* path_h, const float* grad_out_h, int64_t B, int64_t L, int64_t C,
+                                        int32_t depth, float* grad_path_h, int32_t chunks, void* ws, size_t ws_bytes,
+                                        sig_cuda_stream_t s) {
+    if (!path_h || !grad_out_h || !grad_path_h) return fail(SIG_ERR_INVALID_ARG, "host buffers must be non-null");
+    if (B == 0) return ok();
+    size_t off[5];
+    const size_t need = host_fb_layout(B, L, C, depth, chunks, off);
+    if (need == 0) return fail(SIG_ERR_SHAPE, "bad shape B=%lld L=%lld C=%lld depth=%d chunks=%d", (long long)B,
+                               (long long)L, (long long)C, depth, chunks);
+    if (!ws || ws_bytes < need) return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
+    const int64_t S = sig_channels_checked(C, depth);
+    char* w = static_cast<char*>(ws);
+    float* d_path = reinterpret_cast<float*>(w + off[0]);
+    float* d_go = reinterpret_cast<float*>(w + off[1]);
+    float* d_sig = reinterpret_cast<float*>(w + off[2]);
+    float* d_gp = reinterpret_cast<float*>(w + off[3]);
+    void* d_fws = w + off[4];
+    const size_t fws_bytes = need - off[4];
+    const cudaStream_t cs = (cudaStream_t)s;
+    // copy streams, created once per host thread
+    thread_local cudaStream_t h2d = nullptr, d2h = nullptr;
+    if (!h2d && cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess) return cuda_status(cudaGetLastError(), "stream");
+    if (!d2h && cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess) return cuda_status(cudaGetLastError(), "stream");
+    const int64_t bc = (B + chunks - 1) / chunks;
+    const int n = (int)((B + bc - 1) / bc);
+    std::vector<cudaEvent_t> ev(2 * n + 2);
+    for (auto& e : ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cuda_status(cudaGetLastError(), "event");
+    auto release = [&] {
+        for (auto& e : ev) cudaEventDestroy(e);  // released once pending work completes
+    };
+    // the copies start after everything already queued on the caller's stream
+    cudaEventRecord(ev[2 * n], cs);
+    cudaStreamWaitEvent(h2d, ev[2 * n], 0);
+    cudaStreamWaitEvent(d2h, ev[2 * n], 0);
+    for (int k = 0; k < n; ++k) {
+        const int64_t a = k * bc, b = (a + bc < B) ? a + bc : B;
+        cudaMemcpyAsync(d_path + a * L * C, path_h + a * L * C, (size_t)(b - a) * L * C * sizeof(float),
+                        cudaMemcpyHostToDevice, h2d);
+        cudaMemcpyAsync(d_go + a * S, grad_out_h + a * S, (size_t)(b - a) * S * sizeof(float), cudaMemcpyHostToDevice,
+                        h2d);
+        cudaEventRecord(ev[k], h2d);
+    }
+    for (int k = 0; k < n; ++k) {
+        const int64_t a = k * bc, b = (a + bc < B) ? a + bc : B;
+        cudaStreamWaitEvent(cs, ev[k], 0);
+        sig_status_t st = run_signature(d_path + a * L * C, b - a, L, C, depth, 0, SIG_BP_NONE, nullptr, d_sig + a * S,
+                                        d_fws, fws_bytes, cs);
+        if (st == SIG_OK)
+            st = sig_signature_backward(d_go + a * S, d_path + a * L * C, d_sig + a * S, b - a, L, C, depth, 0,
+                                        SIG_BP_NONE, nullptr, d_gp + a * L * C, nullptr, s);
+        if (st != SIG_OK) {
+            release();
+            return st;
+        }
+        cudaEventRecord(ev[n + k], cs);
+        cudaStreamWaitEvent(d2h, ev[n + k], 0);
+        cudaMemcpyAsync(grad_path_h + a * L * C, d_gp + a * L * C, (size_t)(b - a) * L * C * sizeof(float),
+                        cudaMemcpyDeviceToHost, d2h);
+    }
+    // the caller's stream resumes after the last read-back
+    cudaEventRecord(ev[2 * n + 1], d2h);
+    cudaStreamWaitEvent(cs, ev[2 * n + 1], 0);
+    release();
+    return cuda_status(cudaGetLastError(), "host pipeline");
+}
+
 sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, int64_t C, int32_t depth, float* out,
                                    sig_cuda_stream_t s) {
     const int64_t S = sig_channels_checked(C, depth);

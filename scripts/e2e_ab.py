@@ -44,6 +44,9 @@ for k in (2, 4, 8):
     p = HostPipeline([x, g], out, chunks=k)
     t = timeit(lambda: p.run(fn))
     print(f"pipeline x{k}: {t:.3f} ms  {B / t * 1e3:.0f} paths/s")
+for k in (2, 4, 8):
+    t = timeit(lambda: sb.sig_signature_fwd_bwd_host(x, g, N, chunks=k, grad_path_h=out))
+    print(f"native x{k}: {t:.3f} ms  {B / t * 1e3:.0f} paths/s")
 h = torch.empty(157581312 // 4).pin_memory()
 d = torch.empty_like(h, device="cuda")
 t = timeit(lambda: d.copy_(h, non_blocking=True))
