@@ -133,7 +133,7 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
         const int cp = (int)sigb200::ipow(C, pl.P);
         int upc = cp <= 512 ? 512 / cp : 0;
         if (upc > 32) upc = 32;
-        while (upc >= 2 && (size_t)upc * S * sizeof(float) > 200 * 1024) --upc;
+        while (upc >= 2 && (size_t)(upc + (upc + 1) / 2) * S * sizeof(float) > 200 * 1024) --upc;
         if (upc >= 2) {
             pl.upc = upc;
             // one CTA per group of upc chunks: make the CTA count a whole number of waves

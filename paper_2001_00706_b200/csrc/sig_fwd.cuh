@@ -195,6 +195,53 @@ __device__ __forceinline__ void load_state(const float* row, int prefix, float (
     });
 }
 
+// (a [x] b) at flat coefficient f with compile-time shapes (cf. mul_coef in combine.cuh): the level
+// of f selects an unrolled sum whose word splits are divisions by compile-time powers of C.
+template <class SH>
+__device__ __forceinline__ float mul_coef_t(const float* a, const float* b, int f) {
+    constexpr int C = SH::C;
+    float r = 0.0f;
+    static_for<1, SH::N + 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        if (f >= (int)SH::lvl_off(k) && f < (int)SH::lvl_off(k + 1)) {
+            const int w = f - (int)SH::lvl_off(k);
+            float acc = a[f] + b[f];
+            static_for<1, k>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                constexpr int D = (int)ipow(C, k - i);
+                const int u = w / D, v = w - u * D;
+                acc = fmaf(a[(int)SH::lvl_off(i) + u], b[(int)SH::lvl_off(k - i) + v], acc);
+            });
+            r = acc;
+        }
+    });
+    return r;
+}
+
+// Ordered tree fold of cnt signatures gs[0..cnt) (time order) with one barrier per tree level:
+// level results are written compactly into the other buffer (ping-pong gs <-> tmp, tmp holding
+// ceil(cnt/2) signatures).  Returns the buffer holding the product.
+template <class SH>
+__device__ __forceinline__ const float* block_fold_t(float* gs, float* tmp, int cnt) {
+    constexpr int S = (int)SH::S;
+    float* src = gs;
+    float* dst = tmp;
+    while (cnt > 1) {
+        const int np = (cnt + 1) / 2;
+        for (int e = threadIdx.x; e < np * S; e += blockDim.x) {
+            const int pr = e / S, f = e - pr * S;
+            const float* x = src + (size_t)(2 * pr) * S;
+            dst[e] = (2 * pr + 1 < cnt) ? mul_coef_t<SH>(x, x + S, f) : x[f];
+        }
+        __syncthreads();
+        float* t = src;
+        src = dst;
+        dst = t;
+        cnt = np;
+    }
+    return src;
+}
+
 template <class SH>
 __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     constexpr int C = SH::C;
@@ -295,9 +342,9 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
         __syncthreads();
         store_state<SH, false>(zs + (size_t)ul * SH::S, prefix, own, low);
         __syncthreads();
-        block_tree_combine(zs, nu, prm.dims);
+        const float* prod = block_fold_t<SH>(zs, zs + (size_t)nu * SH::S, nu);
         float* o = prm.out + (size_t)blockIdx.x * SH::S;
-        for (int f = threadIdx.x; f < (int)SH::S; f += blockDim.x) o[f] = zs[f];
+        for (int f = threadIdx.x; f < (int)SH::S; f += blockDim.x) o[f] = prod[f];
         return;
     }
     if (valid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
@@ -582,7 +629,9 @@ cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     while (tile > 8 && (size_t)nu * tile * SH::C * 4 > 48 * 1024) tile /= 2;
     prm.tile = tile;
     size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
-    if (prm.upc > 0 && (size_t)nu * SH::S * sizeof(float) > smem) smem = (size_t)nu * SH::S * sizeof(float);
+    // grouped chunks: nu unit signatures plus the fold's second buffer of ceil(nu / 2)
+    if (prm.upc > 0 && (size_t)(nu + (nu + 1) / 2) * SH::S * sizeof(float) > smem)
+        smem = (size_t)(nu + (nu + 1) / 2) * SH::S * sizeof(float);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(sig_fwd_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
