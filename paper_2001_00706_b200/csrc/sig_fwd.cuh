@@ -17,6 +17,15 @@
 #include "combine.cuh"
 #include "sig_common.cuh"
 
+// increments staged per tile of the grouped-chunk scan (at most SIG_FWD_TILE steps and
+// SIG_FWD_TILE_KB of shared memory for all units of the CTA)
+#ifndef SIG_FWD_TILE
+#define SIG_FWD_TILE 1024
+#endif
+#ifndef SIG_FWD_TILE_KB
+#define SIG_FWD_TILE_KB 160
+#endif
+
 namespace sigb200 {
 
 struct FwdParams {
@@ -625,8 +634,13 @@ cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     }
     const int64_t grid = (threads + bd - 1) / bd;
     const int nu = (prm.upc > 0) ? prm.upc : (int)((bd - 1) / SH::CP + 2);  // max units touched by one CTA
-    int tile = (int)(prm.chunk_len < 256 ? prm.chunk_len : 256);
-    while (tile > 8 && (size_t)nu * tile * SH::C * 4 > 48 * 1024) tile /= 2;
+    // grouped chunks (one resident CTA per SM anyway) stage a whole chunk at once: one load phase
+    // and one barrier per CTA instead of one per 128 steps (c5 596 -> 504 us); other scans keep
+    // 48 KB so that small CTAs still fit several per SM
+    const int tmax = prm.upc > 0 ? SIG_FWD_TILE : 256;
+    const size_t tkb = prm.upc > 0 ? SIG_FWD_TILE_KB : 48;
+    int tile = (int)(prm.chunk_len < tmax ? prm.chunk_len : tmax);
+    while (tile > 8 && (size_t)nu * tile * SH::C * 4 > tkb * 1024) tile /= 2;
     prm.tile = tile;
     size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
     // grouped chunks: nu unit signatures plus the fold's second buffer of ceil(nu / 2)
