@@ -131,7 +131,9 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
     if (pl.n_chunks > 1) {
         // group chunks so that each scan CTA folds upc consecutive chunks of one path itself
         const int cp = (int)sigb200::ipow(C, pl.P);
-        int upc = cp <= 512 ? 512 / cp : 0;
+        // ~256-thread CTAs: two or more resident per SM, so one CTA's staging and fold phases
+        // overlap another's scan (c5: 9 chunks of 27 threads, 506 -> 474 us vs 18 per CTA)
+        int upc = cp <= 256 ? 256 / cp : 0;
         if (upc > 32) upc = 32;
         while (upc >= 2 && (size_t)(upc + (upc + 1) / 2) * S * sizeof(float) > 200 * 1024) --upc;
         if (upc >= 2) {
