@@ -75,7 +75,16 @@ struct FwdPlan {
     size_t ws_bytes;
 };
 
-int group_size_for(int64_t S) {
+int group_size_for(int64_t S, bool compiled) {
+    if (compiled) {
+        // compiled fold (fold_group_t_kernel, one barrier per tree level, 512 threads): small groups
+        // and many CTAs per level -- each CTA's fold is latency-bound (c5, 740 partials: G = 4, 8,
+        // 16 measured 432, 435, 444 us for the whole signature)
+        int G = 4;
+        while (G > 2 && (size_t)(G + (G + 1) / 2) * S * sizeof(float) > 200 * 1024) G >>= 1;
+        if ((size_t)(G + (G + 1) / 2) * S * sizeof(float) <= 200 * 1024) return G;
+        return 0;
+    }
     // small groups: many CTAs, few loads per thread (the fold is latency-bound, not FLOP-bound)
     int G = 8;
     while (G > 2 && (size_t)G * S * sizeof(float) > 200 * 1024) G >>= 1;
@@ -83,9 +92,9 @@ int group_size_for(int64_t S) {
     return G;
 }
 
-void plan_fold(int64_t n, int64_t S, int64_t B, int& G, int64_t* lv, int& nl, size_t& elems) {
+void plan_fold(int64_t n, int64_t S, int64_t B, int& G, int64_t* lv, int& nl, size_t& elems, bool compiled) {
     // n elements per path -> ... -> 1; intermediate results go to the workspace (the last to out)
-    G = group_size_for(S);
+    G = group_size_for(S, compiled);
     const int g = G > 0 ? G : 2;
     nl = 0;
     elems = 0;
@@ -153,7 +162,7 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
     pl.n_fold = 0;
     pl.G = 0;
     if (pl.n_chunks > 1) {
-        if (pl.n_parts > 1) plan_fold(pl.n_parts, S, B, pl.G, pl.fold_levels, pl.n_fold, elems);
+        if (pl.n_parts > 1) plan_fold(pl.n_parts, S, B, pl.G, pl.fold_levels, pl.n_fold, elems, ks->fold != nullptr);
         elems += (size_t)pl.n_parts * B * S;  // the (partial) chunk signatures themselves
     }
     pl.ws_bytes = elems * sizeof(float);
@@ -162,13 +171,13 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
 
 // fold n elements per path (element (j, b) at in + j*sj + b*sb) into out[b] (row stride S)
 cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_t sb, int64_t n, int64_t B, float* out,
-                        float* ws, cudaStream_t st) {
+                        float* ws, cudaStream_t st, FoldLaunch tf = nullptr) {
     const int64_t S = d.S;
     if (n == 1) {
         return cudaMemcpy2DAsync(out, S * sizeof(float), in, sb * sizeof(float), S * sizeof(float), B,
                                  cudaMemcpyDeviceToDevice, st);
     }
-    int G = group_size_for(S);
+    int G = group_size_for(S, tf != nullptr);
     const float* cur = in;
     int64_t csj = sj, csb = sb;
     float* buf = ws;
@@ -198,6 +207,16 @@ cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_
             gp.out = dst;
             gp.out_sj = dsj;
             gp.out_sb = dsb;
+            if (tf) {
+                cudaError_t e = tf(gp, (unsigned)ng, (unsigned)B, st);
+                if (e != cudaSuccess) return e;
+                count_launch();
+                cur = dst;
+                csj = dsj;
+                csb = dsb;
+                n = ng;
+                continue;
+            }
             const size_t smem = (size_t)G * S * sizeof(float);
             if (smem > 48 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(combine_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -281,7 +300,7 @@ sig_status_t run_signature(const float* path, int64_t B, int64_t L, int64_t C, i
     if (pl.n_chunks > 1 && pl.n_parts > 1) {
         // part (b, j) at units + (b*n_parts + j)*S  ->  element (j, b): sj = S, sb = n_parts*S
         float* fold_ws = units + (size_t)pl.n_parts * B * d.S;
-        e = launch_fold(d, units, d.S, pl.n_parts * d.S, pl.n_parts, B, out, fold_ws, s);
+        e = launch_fold(d, units, d.S, pl.n_parts * d.S, pl.n_parts, B, out, fold_ws, s, pl.ks->fold);
         if (e != cudaSuccess) return cuda_status(e, "chunk fold launch");
     }
     return ok();
@@ -873,7 +892,8 @@ size_t sig_multi_signature_combine_workspace_size(int64_t n, int64_t B, int64_t 
     int64_t lv[64];
     int nl;
     size_t elems;
-    plan_fold(n, S, B, G, lv, nl, elems);
+    const KernelSet* ks = (C <= 8) ? find_kernels((int)C, depth) : nullptr;
+    plan_fold(n, S, B, G, lv, nl, elems, ks && ks->fold);
     return elems * sizeof(float);
 }
 
@@ -889,7 +909,9 @@ sig_status_t sig_multi_signature_combine(const float* sigs, int64_t n, int64_t B
         return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);
     if (B == 0) return ok();
     const TensorDims d = make_dims((int)C, depth);
-    cudaError_t e = launch_fold(d, sigs, B * S, S, n, B, out, static_cast<float*>(ws), (cudaStream_t)s);
+    const KernelSet* ks = (C <= 8) ? find_kernels((int)C, depth) : nullptr;
+    cudaError_t e = launch_fold(d, sigs, B * S, S, n, B, out, static_cast<float*>(ws), (cudaStream_t)s,
+                                ks ? ks->fold : nullptr);
     return cuda_status(e, "multi combine launch");
 }
 

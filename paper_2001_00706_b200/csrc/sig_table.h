@@ -7,10 +7,12 @@ namespace sigb200 {
 
 struct FwdParams;
 struct BwdParams;
+struct GroupParams;
 
 using FwdLaunch = cudaError_t (*)(const FwdParams&, cudaStream_t);
 using BwdLaunch = cudaError_t (*)(const BwdParams&, cudaStream_t);
 using BwdMaxChunk = int64_t (*)();
+using FoldLaunch = cudaError_t (*)(const GroupParams&, unsigned ngroups, unsigned B, cudaStream_t);
 
 struct KernelSet {
     int C, N;
@@ -18,6 +20,7 @@ struct KernelSet {
     FwdLaunch fwd0, fwd1;
     BwdLaunch bwd;
     BwdMaxChunk bwd_max_chunk;  // longest time chunk the backward stages in shared memory
+    FoldLaunch fold;            // compiled ordered group fold (K3) for this (C, N)
 };
 
 const KernelSet* kernels_c1(int N);

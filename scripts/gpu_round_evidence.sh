@@ -18,4 +18,8 @@ ncu --set full --clock-control none --import-source on -k regex:sig_fwd_stream_k
     python scripts/profile_c2.py c3 3 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sig_bwd_kernel -s 1 -c 1 -o gpurun_out/c4_k2_full \
     python scripts/profile_c2.py c4 3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sig_fwd_kernel -s 1 -c 1 -o gpurun_out/c5_k1_full \
+    python scripts/profile_c2.py c5 3 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv \
+    python bench.py --config c5 --steps 8 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ls -la gpurun_out
