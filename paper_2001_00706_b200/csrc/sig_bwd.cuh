@@ -400,6 +400,22 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
         for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
         for (int j = 0; j < jn; ++j) {
             const int64_t t = M - 1 - (n0 + j);
+            if constexpr (STREAM) {
+                // stream mode adds a grad_out row per step: no room to carry the previous gz
+                // through the step, reduce it first
+                float v[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) v[c] = gz[c];
+                reduce_a(v);
+                reduce_c(reduce_b(v, acc), v, acc, j - 1);
+                stream_add(t);
+                float z[C], zp[SH::PD];
+                load_z(t, z, zp);
+                fused_mulexp<SH, N - 1, true>(A, low, z, zp);
+                chains_lower(z, zp, gz, acc);
+                chain_top(z, zp, gz, acc);
+                continue;
+            }
             stream_add(t);
             float z[C], zp[SH::PD];
             load_z(t, z, zp);
