@@ -194,3 +194,14 @@ def test_logsignature_inverse(stream):
     ref = -oracle.logsignature(x, N, mode="expand", stream=stream)
     S = ref.shape[-1]
     assert level_rel_err(inv.reshape(-1, S), ref.reshape(-1, S), C, N) < FWD_TOL
+
+
+@pytest.mark.parametrize("C,N,n", [(8, 4, 7), (8, 5, 3), (2, 9, 17)])
+def test_multi_combine_fold_paths(C, N, n):
+    """The compiled group fold (S small enough for groups in shared memory: (8,4), (2,9)) and the
+    pairwise fold in global memory (S = 37448 at (8,5)) against the oracle's left fold."""
+    B = 2
+    sigs = np.stack([oracle.signature(brownian_paths(B, 6, C, seed=100 + j), N) for j in range(n)]).astype(np.float32)
+    got = sb.multi_signature_combine(_cuda(sigs), C, N).cpu().numpy()
+    ref = oracle.multi_combine(sigs, C, N)
+    assert level_rel_err(got, ref, C, N) < FWD_TOL
