@@ -104,7 +104,10 @@ sig_status_t sig_signature(const float* path, int64_t B, int64_t L, int64_t C, i
  *                  reversal eq-reverse); consistency with `path` is NOT checked
  *   grad_path      [B, L, C], overwritten
  *   grad_basepoint [B, C] (bp == SIG_BP_GIVEN) or NULL; overwritten when given
- * Needs the increments of one path in shared memory: M * C <= 32768 floats, else UNSUPPORTED. */
+ * One CTA reverses one path and stages its increments in shared memory; a path longer than that
+ * (about 227 KB of increments, shape-dependent) needs the time-parallel backward and its workspace:
+ * this call then returns SIG_ERR_WORKSPACE -- use sig_signature_backward_ex with
+ * sig_signature_backward_ex_workspace_size(...) bytes. */
 sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
                                     int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
                                     const float* basepoint, float* grad_path, float* grad_basepoint,
@@ -124,7 +127,8 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
  *   grad_path_h  [B, L, C] host, written
  *   ws           device workspace of sig_signature_fwd_bwd_host_workspace_size(...) bytes (holds the
  *                device copies of the inputs, the signatures, the gradients; caller-owned)
- * No basepoint, no stream mode.  Returns the first failing call's status. */
+ * No basepoint, no stream mode; each path must fit the plain backward (see sig_signature_backward).
+ * Returns the first failing call's status. */
 size_t sig_signature_fwd_bwd_host_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t chunks);
 sig_status_t sig_signature_fwd_bwd_host(const float* path_h, const float* grad_out_h, int64_t B, int64_t L, int64_t C,
                                         int32_t depth, float* grad_path_h, int32_t chunks, void* ws, size_t ws_bytes,
