@@ -50,17 +50,23 @@ def alg_flops(op: str, B: int, M: int, C: int, N: int) -> float:
     return (4.0 * fused_cost(C, N) + 2.0 * fused_cost(C, N - 1)) * M * B
 
 
-def fp32_peak_tflops() -> tuple[float, str]:
+def fp32_peak_tflops() -> tuple[float, str, float | None]:
     """FP32 FMA peak: 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz (max SM clock in
     MEASURED_PEAKS.json) = 74.45 TFLOP/s.  MEASURED_PEAKS.json carries no FP32 figure; DESIGN.md
-    derives this denominator from the guide's unit counts and clocks."""
+    derives this denominator from the guide's unit counts and clocks.  The third value is the
+    FFMA microbenchmark's measured peak on this pool (profiles/fp32_peak.json), reported beside it."""
     mhz = 1965.0
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         mhz = float(mp.get("sm_max_mhz", mhz))
     except Exception:
         pass
-    return 148 * 128 * 2 * mhz * 1e6 / 1e12, f"148 SM x 128 lanes x 2 x {mhz:.0f} MHz (derived, DESIGN.md)"
+    meas = None
+    try:
+        meas = float(json.load(open(os.path.join(ROOT, "profiles", "fp32_peak.json")))["tflops"])
+    except Exception:
+        pass
+    return (148 * 128 * 2 * mhz * 1e6 / 1e12, f"148 SM x 128 lanes x 2 x {mhz:.0f} MHz (derived, DESIGN.md)", meas)
 
 
 class ClockSampler:
@@ -209,62 +215,103 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(name, world):
+def _config_dict(name, world, scaling="weak", B=None, l2=None):
     cfg = CONFIGS[name]
-    return {"workload": f"{name}: {cfg['op']} B={cfg['B']}/GPU L={cfg['L']} C={cfg['C']} N={cfg['N']}"
+    B = B or cfg["B"]
+    if name == "c5":
+        par = f"time-chunk x{world} (NCCL all-gather + ordered fold)" if world > 1 else "single GPU"
+        bdesc = "B=1"
+    elif scaling == "strong":
+        par = f"batch-shard x{world}, global batch {B} (rank r: dist.batch_bounds)" if world > 1 else "single GPU"
+        bdesc = f"B={B} global"
+    else:
+        par = f"batch-shard x{world}, {B} paths per GPU" if world > 1 else "single GPU"
+        bdesc = f"B={B}/GPU"
+    return {"workload": f"{name}: {cfg['op']} {bdesc} L={cfg['L']} C={cfg['C']} N={cfg['N']}"
                         f"{' stream' if cfg['stream'] else ''}, Brownian",
-            "B_per_gpu": cfg["B"], "L": cfg["L"], "C": cfg["C"], "depth": cfg["N"], "stream": cfg["stream"],
-            "parallelism": (f"time-chunk x{world} (NCCL all-gather + ordered fold)" if name == "c5" else
-                            f"batch-shard x{world}") if world > 1 else "single GPU",
-            "l2": "per-step working set > 126 MB L2 (grad_out + signature 307 MB); no flush needed"
-            if name == "c2" else "see DESIGN.md"}
+            "B_per_gpu" if scaling != "strong" else "B_global": B, "L": cfg["L"], "C": cfg["C"],
+            "depth": cfg["N"], "stream": cfg["stream"], "parallelism": par, "scaling": scaling,
+            "l2": l2 or ("per-step working set > 126 MB L2 (grad_out + signature 307 MB); no flush needed"
+                         if name == "c2" else "see DESIGN.md")}
 
 
 # ------------------------------------------------------------------------------------------------
+L2_BYTES = 126 * 2 ** 20
+
+
 class Workload:
     """One BASELINE config as a benchmark step.  step(ev) runs one step on the device (ev: list of
-    (label, start_event, end_event) for the live per-kernel split, or None); e2e_step() runs it from
-    pinned host buffers; units = paths processed per step on this rank."""
+    (label, event) marks for the live per-segment split, or None); e2e_step() runs it from pinned
+    host buffers; units = paths this rank processes per step.
 
-    def __init__(self, name, rank, world, dev):
+    scaling: "weak" -- every rank its own batch of B paths (B = the config's, or --batch);
+             "strong" -- one global batch of B paths, rank r takes [rB/G, (r+1)B/G) (dist.batch_bounds);
+    c5 is always time-chunked over the ranks (one path per step for the whole job)."""
+
+    def __init__(self, name, rank, world, dev, scaling="weak", batch=None):
         import torch
 
         import paper_2001_00706_b200 as sb
+        from paper_2001_00706_b200 import dist as sdist
 
         self.sb, self.torch, self.dev, self.name = sb, torch, dev, name
         cfg = CONFIGS[name]
         self.cfg = cfg
-        self.B, self.L, self.C, self.N = cfg["B"], cfg["L"], cfg["C"], cfg["N"]
+        self.L, self.C, self.N = cfg["L"], cfg["C"], cfg["N"]
         self.S = sb.sig_signature_channels(self.C, self.N)
         ps, gs = SEEDS[name]
         self.world, self.rank = world, rank
+        self.scaling = "strong" if name == "c5" else scaling
+        B0 = int(batch) if batch else cfg["B"]
         if name == "c5":
-            from paper_2001_00706_b200 import dist as sdist
-
             full = brownian_paths(1, self.L, self.C, ps)  # the one long path, time-chunked over ranks
             a, b = sdist.time_chunk_bounds(self.L, world, rank)
             self.x_np = np.ascontiguousarray(full[:, a:b])
             self.M = b - a - 1
+            self.B = 1
+            self.B_global = 1
             self.units = 1.0 / world  # one path per step for the whole job
+            self.gsl = slice(0, 1)
+        elif self.scaling == "strong":
+            lo, hi = sdist.batch_bounds(B0, world, rank)
+            self.x_np = np.ascontiguousarray(brownian_paths(B0, self.L, self.C, ps)[lo:hi])
+            self.B, self.B_global, self.M = hi - lo, B0, self.L - 1
+            self.units = float(self.B)
+            self.gsl = slice(lo, hi)
         else:
-            self.x_np = brownian_paths(self.B, self.L, self.C, ps + 7919 * rank)
-            self.M = self.L - 1
-            self.units = self.B
+            self.x_np = brownian_paths(B0, self.L, self.C, ps + 7919 * rank)
+            self.B, self.B_global, self.M = B0, B0 * world, self.L - 1
+            self.units = float(B0)
+            self.gsl = slice(0, B0)
         self.x = torch.from_numpy(self.x_np).to(dev)
         self.g = None
+        gseed = (gs or 0) + (7919 * rank if self.scaling == "weak" else 0)
         if cfg["op"] == "sig_fwd_bwd":
-            self.g_np = normal((self.B, self.S), gs + 7919 * rank)
+            self.g_np = normal((B0, self.S), gseed)[self.gsl]
         elif cfg["op"] == "logsig_words_fwd_bwd":
-            self.g_np = normal((self.B, sb.sig_logsignature_channels(self.C, self.N, "words")), gs + 7919 * rank)
+            self.g_np = normal((B0, sb.sig_logsignature_channels(self.C, self.N, "words")), gseed)[self.gsl]
         else:
             self.g_np = None
         if self.g_np is not None:
+            self.g_np = np.ascontiguousarray(self.g_np)
             self.g = torch.from_numpy(self.g_np).to(dev)
         self.stream = torch.cuda.current_stream(dev)
+        # per-step working set: inputs larger than L2 need no flush between timed steps
+        ws = self.x.numel() * 4 + (self.g.numel() * 4 if self.g is not None else 0)
+        if cfg["op"] == "sig_fwd_bwd":
+            ws += self.B * self.S * 4 * 2
+        elif cfg["op"] == "sig_fwd_stream":
+            ws += self.B * self.M * self.S * 4
+        elif cfg["op"] == "logsig_words_fwd_bwd":
+            ws += self.B * self.S * 4 * 4
+        self.working_set = ws
+        self.flush = ws <= L2_BYTES
+        self.l2 = (f"per-step working set {ws / 1e6:.0f} MB > 126 MB L2; no flush needed" if not self.flush else
+                   f"per-step working set {ws / 1e6:.1f} MB < L2: L2 flushed (256 MB write) before every timed step, "
+                   f"outside the per-step events")
 
     def _run(self, x, g, ev):
         sb, N, torch = self.sb, self.N, self.torch
-        rec = (lambda lab: ev.append((lab, torch.cuda.Event(enable_timing=True)))) if ev is not None else None
 
         def mark(lab):
             if ev is not None:
@@ -292,7 +339,6 @@ class Workload:
         else:
             res = sb.sig_signature(x, N, stream=self.cfg["stream"])
             mark("fwd")
-        del rec
         return res
 
     def step(self, ev=None):
@@ -328,26 +374,28 @@ class Workload:
 
     def roofline(self, seg_ms, ms_step):
         """Dominant kernel's roofline from the live per-segment CUDA-event times."""
-        C, N, M, B = self.C, self.N, self.M, (1 if self.name == "c5" else self.B)
-        peak, peak_src = fp32_peak_tflops()
+        C, N, M, B = self.C, self.N, self.M, self.B
+        peak, peak_src, peak_meas = fp32_peak_tflops()
         op = self.cfg["op"]
-        traffic = None
         try:
             traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(self.name, {})
         except Exception:
             traffic = {}
+        meas = (lambda a: {"peak_measured": peak_meas, "frac_of_measured": a / peak_meas} if peak_meas else {})
         if op in ("sig_fwd_bwd", "logsig_words_fwd_bwd"):
             f_fwd = alg_flops("fwd", B, M, C, N)
             f_bwd = alg_flops("bwd", B, M, C, N)
             ach = f_bwd / (seg_ms["bwd"] / 1000) / 1e12
-            kern = ("sig_bwd2_kernel (reversible backward, two prefixes per thread)" if op == "sig_fwd_bwd"
+            kern = ("sig_bwd2p_kernel (reversible backward, sibling prefixes packed per FFMA2)" if op == "sig_fwd_bwd"
                     else "sig_logsignature_backward call = logsig_bwd_kernel + sig_bwd_kernel (sig-bwd FLOPs only)")
-            return {"bound": "alu", "kernel": kern, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": traffic.get("sig_bwd_kernel"), "peak_source": peak_src,
-                    "kernel_ms": seg_ms["bwd"], "step_share": seg_ms["bwd"] / (seg_ms["fwd"] + seg_ms["bwd"]),
-                    "fwd": {"kernel_ms": seg_ms["fwd"], "achieved": f_fwd / (seg_ms["fwd"] / 1000) / 1e12,
-                            "frac": f_fwd / (seg_ms["fwd"] / 1000) / 1e12 / peak},
-                    "step_frac": (f_fwd + f_bwd) / (ms_step / 1000) / 1e12 / peak}
+            r = {"bound": "alu", "kernel": kern, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                 "frac": ach / peak, "traffic": traffic.get("sig_bwd_kernel"), "peak_source": peak_src,
+                 "kernel_ms": seg_ms["bwd"], "step_share": seg_ms["bwd"] / (seg_ms["fwd"] + seg_ms["bwd"]),
+                 "fwd": {"kernel_ms": seg_ms["fwd"], "achieved": f_fwd / (seg_ms["fwd"] / 1000) / 1e12,
+                         "frac": f_fwd / (seg_ms["fwd"] / 1000) / 1e12 / peak},
+                 "step_frac": (f_fwd + f_bwd) / (ms_step / 1000) / 1e12 / peak}
+            r.update(meas(ach))
+            return r
         if op == "sig_fwd_stream":
             hbm = 6543.7
             try:
@@ -356,14 +404,18 @@ class Workload:
                 pass
             nbytes = B * M * self.S * 4 + B * self.L * C * 4  # written prefixes + read path
             ach = nbytes / (seg_ms["fwd"] / 1000) / 1e9
-            return {"bound": "hbm", "kernel": "sig_fwd_stream_kernel (stream=True, staged rows + TMA bulk stores)", "achieved": ach, "peak": hbm,
-                    "unit": "GB/s", "frac": ach / hbm, "traffic": traffic.get("sig_fwd_kernel"),
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel_ms": seg_ms["fwd"]}
+            return {"bound": "hbm", "kernel": "sig_fwd_stream_kernel (stream=True, staged rows + TMA bulk stores)",
+                    "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": traffic.get("sig_fwd_kernel"), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "kernel_ms": seg_ms["fwd"]}
         f = alg_flops("fwd", B, M, C, N)
         ach = f / (seg_ms["fwd"] / 1000) / 1e12
-        return {"bound": "alu", "kernel": "sig_fwd_kernel (+ ordered chunk fold" + (", NCCL all-gather)" if self.world > 1 else ")"),
-                "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": traffic.get("sig_fwd_kernel"), "peak_source": peak_src, "kernel_ms": seg_ms["fwd"]}
+        r = {"bound": "alu",
+             "kernel": "sig_fwd_kernel (+ ordered chunk fold" + (", NCCL all-gather)" if self.world > 1 else ")"),
+             "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+             "traffic": traffic.get("sig_fwd_kernel"), "peak_source": peak_src, "kernel_ms": seg_ms["fwd"]}
+        r.update(meas(ach))
+        return r
 
 
 def bind_gpu_local_cpus(index: int):
@@ -389,74 +441,109 @@ def bind_gpu_local_cpus(index: int):
     return None
 
 
-def run_ours(args, rank: int, world: int):
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _max_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
     import torch
     import torch.distributed as dist
 
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def time_workload(wl, steps: int, warmup: int, world: int, dev, split_every: int = 4, sampler=None):
+    """W untimed warm-up steps, then K timed steps bracketed by barrier + synchronize, CUDA events on
+    the launching stream.  Returns ms per step (block time / K, max over ranks), the per-step times
+    (min / median, per-step events), the live per-segment split and the library launches."""
+    import torch
+
     import paper_2001_00706_b200 as sb
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
-    all_cpus = os.sched_getaffinity(0)
-    bind_gpu_local_cpus(dev.index)
-    torch.cuda.set_device(dev)
-    wl = Workload(args.config, rank, world, dev)
     stream = wl.stream
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
-    for _ in range(args.warmup):
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if wl.flush else None
+    for _ in range(warmup):
         wl.step()
     torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+    _barrier(world)
     torch.cuda.synchronize(dev)
     launches0 = sb.lib().sig_launch_count()
-    splits = []
-    sampler = ClockSampler(dev.index)
-    with sampler:
+    marks, splits = [], []
+    import contextlib
+
+    with (sampler if sampler is not None else contextlib.nullcontext()):
         t_start, t_end = ev(), ev()
         t_start.record(stream)
-        for i in range(args.steps):
-            if i % 4 == 0:
+        for i in range(steps):
+            if flush is not None:
+                flush.zero_()  # evict the previous step's data from L2 (outside the per-step events)
+            a, b = ev(), ev()
+            a.record(stream)
+            if split_every and i % split_every == 0:
                 rec = []
                 wl.step(rec)
                 splits.append(rec)
             else:
                 wl.step()
+            b.record(stream)
+            marks.append((a, b))
         t_end.record(stream)
         torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+    _barrier(world)
     torch.cuda.synchronize(dev)
     launches = sb.lib().sig_launch_count() - launches0
-    ms_t = torch.tensor([t_start.elapsed_time(t_end)], device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_step = float(ms_t.item()) / args.steps
-    value = world * wl.units / (ms_step / 1000.0)
+    per_step = [a.elapsed_time(b) for a, b in marks]
+    # with flushes between steps the block time includes them: the step time is the sum of the steps
+    block = sum(per_step) if flush is not None else t_start.elapsed_time(t_end)
+    ms_step = _max_over_ranks(block, world, dev) / steps
     seg = {}
     for rec in splits:
         for (la, ea), (lb, eb) in zip(rec, rec[1:]):
             seg.setdefault(lb, []).append(ea.elapsed_time(eb))
     seg_ms = {k: float(np.mean(v)) for k, v in seg.items()}
-    roofline = wl.roofline(seg_ms, ms_step)
+    return {"ms_step": ms_step, "ms_min": _max_over_ranks(float(np.min(per_step)), world, dev),
+            "ms_median": _max_over_ranks(float(np.median(per_step)), world, dev), "seg_ms": seg_ms,
+            "launches": int(launches)}
 
-    # ---- e2e through the C ABI from pinned host buffers (H2D inputs, D2H result, every step)
+
+def measure_e2e(wl, steps: int, world: int, dev):
+    """The same step through the C ABI from pinned host buffers (H2D inputs, D2H result, every step)."""
+    import torch
+
+    stream = wl.stream
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     wl.prepare_e2e()
-    n_e2e = max(3, min(args.steps, 50))
+    n_e2e = max(3, min(steps, 50))
     for _ in range(10):  # the first passes over fresh pinned buffers run slow
         wl.e2e_step()
     torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+    _barrier(world)
     a, b = ev(), ev()
     a.record(stream)
     for _ in range(n_e2e):
         wl.e2e_step()
     b.record(stream)
     torch.cuda.synchronize(dev)
-    e_ms = torch.tensor([a.elapsed_time(b) / n_e2e], device=dev)
-    if world > 1:
-        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e_ms = _max_over_ranks(a.elapsed_time(b) / n_e2e, world, dev)
     # context for the e2e number: the plain pinned H2D bandwidth of this box, same buffers (it varied
     # 37-55 GB/s between boxes and runs during development)
     src = wl.gh if wl.gh is not None else wl.xh
@@ -469,42 +556,147 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize(dev)
     h2d_gbs = 3 * src.numel() * 4 / (a.elapsed_time(b) / 1000) / 1e9
     del dst
-    e2e = {"value": world * wl.units / (float(e_ms.item()) / 1000), "unit": UNIT,
-           "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),
-           "h2d_gbs_probe": round(h2d_gbs, 1),
-           "path": ("C ABI calls from pinned host buffers (inputs H2D, result D2H inside the timed region)" +
-                    ("; sig_signature_fwd_bwd_host: one C-ABI call on the host buffers, 4 batch slices whose copies "
-                     "overlap the kernels"
-                     if wl.pipe is not None else ""))}
+    units = _sum_over_ranks(wl.units, world, dev)
+    return {"value": units / (e_ms / 1000), "unit": UNIT,
+            "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),
+            "h2d_gbs_probe": round(h2d_gbs, 1),
+            "path": ("C ABI calls from pinned host buffers (inputs H2D, result D2H inside the timed region)" +
+                     ("; sig_signature_fwd_bwd_host: one C-ABI call on the host buffers, 4 batch slices whose "
+                      "copies overlap the kernels" if wl.pipe is not None else ""))}
 
+
+def _metric_name(name):
+    return METRIC if name == "c2" else f"{CONFIGS[name]['op']} paths/sec ({name})"
+
+
+def measure_config(name, rank, world, dev, steps, warmup, scaling="weak", batch=None):
+    """A bounded measurement of one BASELINE config (the `configs` block and the strong/weak arm)."""
+    wl = Workload(name, rank, world, dev, scaling=scaling, batch=batch)
+    r = time_workload(wl, steps, warmup, world, dev)
+    units = _sum_over_ranks(wl.units, world, dev)
+    out = {"metric": _metric_name(name), "value": units / (r["ms_step"] / 1000), "unit": UNIT,
+           "ms_per_step": r["ms_step"], "ms_min": r["ms_min"], "ms_median": r["ms_median"], "steps": steps,
+           "warmup": warmup, "scaling": wl.scaling,
+           "config": _config_dict(name, world, wl.scaling, wl.B_global if wl.scaling == "strong" else wl.B, wl.l2),
+           "roofline": wl.roofline(r["seg_ms"], r["ms_step"]), "gpu_launches": r["launches"]}
+    del wl
+    return out
+
+
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    all_cpus = os.sched_getaffinity(0)
+    bind_gpu_local_cpus(dev.index)
+    torch.cuda.set_device(dev)
+    wl = Workload(args.config, rank, world, dev, scaling=args.scaling, batch=args.batch)
+    sampler = ClockSampler(dev.index)
+    r = time_workload(wl, args.steps, args.warmup, world, dev, sampler=sampler)
+    ms_step = r["ms_step"]
+    units = _sum_over_ranks(wl.units, world, dev)
+    value = units / (ms_step / 1000.0)
+    roofline = wl.roofline(r["seg_ms"], ms_step)
+    e2e = measure_e2e(wl, args.steps, world, dev)
+    scaling = wl.scaling
+    line = {
+        "metric": _metric_name(args.config),
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "ms_min": r["ms_min"], "ms_median": r["ms_median"],
+        "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config_dict(args.config, world, scaling, wl.B_global if scaling == "strong" else wl.B, wl.l2),
+        "roofline": roofline, "e2e": e2e, "clocks": sampler.summary(), "gpu_launches": r["launches"],
+    }
+    del wl
+    torch.cuda.empty_cache()
+    # the other scaling mode of a batch-sharded config, measured in the same run (at N = 1 both
+    # modes are the same workload)
+    if world > 1 and args.config in ("c2", "c4") and not args.no_configs:
+        other = "strong" if scaling == "weak" else "weak"
+        line[other] = measure_config(args.config, rank, world, dev, min(args.steps, 100), args.warmup,
+                                     scaling=other, batch=args.batch)
+    # every other BASELINE config, bounded, in the same run (c1 is a single-GPU row, SURVEY 8(e))
+    if not args.no_configs:
+        blk = {}
+        for name in ("c1", "c2", "c3", "c4", "c5"):
+            if name == args.config or (name == "c1" and world > 1):
+                continue
+            blk[name] = measure_config(name, rank, world, dev, min(args.steps, 50), args.warmup)
+            torch.cuda.empty_cache()
+        line["configs"] = blk
     if rank != 0:
         return
-    line = {
-        "metric": METRIC if args.config == "c2" else f"{CONFIGS[args.config]['op']} paths/sec ({args.config})",
-        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if args.config == "c5" else "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config_dict(args.config, world),
-        "roofline": roofline, "e2e": e2e, "clocks": sampler.summary(), "gpu_launches": int(launches),
-    }
     if world == 1 and not args.no_cpu_baseline:
         os.sched_setaffinity(0, all_cpus)  # the oracle gets every host core, not just the GPU-local ones
         line["cpu_baseline"] = cpu_baseline(args.config, seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
 
 
+def run_dry(args, rank: int, world: int):
+    """--dry-run: the launch / rendezvous / timing / max-over-ranks / JSON path on CPU (gloo), no
+    kernels and no oracle -- for the CPU tests of the multi-process bench."""
+    import torch
+
+    x = torch.randn(64, 64)
+    ts = []
+    for _ in range(args.warmup):
+        x = torch.tanh(x @ x.T / 64)
+    _barrier(world)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        x = torch.tanh(x @ x.T / 64)
+        ts.append((time.perf_counter() - t0) * 1000)
+    _barrier(world)
+    ms = _max_over_ranks(float(np.sum(ts)), world, torch.device("cpu")) / args.steps
+    if rank == 0:
+        print(json.dumps({"metric": _metric_name(args.config), "dry_run": True, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                          "backend": args.backend, "scaling": args.scaling}), flush=True)
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None, help="ranks (one per GPU); launches them itself if needed")
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="batch-sharded configs: weak = B paths per GPU, strong = B paths over all GPUs")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's batch B (per-shard studies)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default=None)
+    ap.add_argument("--dry-run", action="store_true", help="CPU orchestration check: no kernels, no oracle")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other configs / the other scaling arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    gpus = args.gpus if args.gpus is not None else (int(env_world) if env_world else 1)
+    if env_world is None and gpus > 1:
+        # one process per GPU: re-launch this script under torchrun (rendezvous on 127.0.0.1)
+        import subprocess
+
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+        cmd += sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world = int(env_world or "1")
+    if args.gpus is not None and args.gpus != world:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to measure a different world size")
     rank = int(os.environ.get("RANK", "0"))
+    args.backend = args.backend or ("gloo" if args.dry_run else "nccl")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -512,10 +704,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        if not args.dry_run:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group(args.backend)
     try:
-        run_ours(args, rank, world)
+        (run_dry if args.dry_run else run_ours)(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -112,6 +112,33 @@ def lib():
     return _lib
 
 
+def _on_device(fn):
+    """Run a C-ABI mirror with the CUDA device of its first CUDA tensor argument current: the library
+    launches on the current device, and the stream passed is that tensor's device stream."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        for a in list(args) + list(kwargs.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+
+    return wrapped
+
+
+def _shape(t: torch.Tensor, want: tuple, name: str):
+    if tuple(t.shape) != tuple(want):
+        raise SigError(f"{name} must have shape {list(want)}, got {list(t.shape)}")
+
+
+def _path3(path: torch.Tensor):
+    if path.dim() != 3:
+        raise SigError(f"path must be [B, L, C], got shape {list(path.shape)}")
+    return path.shape
+
+
 def _check(status: int, what: str):
     if status != 0:
         L = lib()
@@ -143,8 +170,13 @@ def _bp(basepoint, path):
     if basepoint is True:
         return BP_ZERO, None
     bp = _dev_f32(basepoint, "basepoint")
+    B, C = path.shape[0], path.shape[-1]
     if bp.dim() == 1:
-        bp = bp.unsqueeze(0).expand(path.shape[0], -1).contiguous()
+        bp = bp.unsqueeze(0)
+    if bp.dim() != 2 or bp.shape[-1] != C or bp.shape[0] not in (1, B):
+        raise SigError(f"basepoint must be [{C}], [1, {C}] or [{B}, {C}], got {list(basepoint.shape)}")
+    if bp.shape[0] != B:
+        bp = bp.expand(B, -1).contiguous()
     return BP_GIVEN, bp
 
 
@@ -163,16 +195,19 @@ def sig_is_supported(C: int, depth: int, backward: bool = False) -> bool:
     return bool(lib().sig_is_supported(C, depth, int(backward)))
 
 
+@_on_device
 def sig_signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=None, inverse: bool = False,
                   initial=None) -> torch.Tensor:
     """sig_signature / sig_signature_ex: inverse and initial as in include/sig.h (reading R18)."""
     path = _dev_f32(path, "path")
-    B, L, C = path.shape
+    B, L, C = _path3(path)
     bpm, bp = _bp(basepoint, path)
     Lib = lib()
     S = Lib.sig_signature_channels(C, depth)
     if S < 0:
         raise SigError(f"bad C={C} depth={depth}")
+    if initial is not None:
+        _shape(initial, (B, S), "initial")
     M = L - 1 + (bpm != BP_NONE)
     out = torch.empty((B, M, S) if stream else (B, S), device=path.device, dtype=torch.float32)
     if not inverse and initial is None:
@@ -197,17 +232,26 @@ def sig_signature_backward(grad_out, path, out_saved, depth: int, stream: bool =
     return gp, gbp
 
 
+@_on_device
 def sig_signature_backward_ex(grad_out, path, out_saved, depth: int, stream: bool = False, basepoint=None,
                               inverse: bool = False, initial=None, want_grad_initial: bool = True):
     """-> (grad_path, grad_basepoint or None, grad_initial or None)."""
     path = _dev_f32(path, "path")
     grad_out = _dev_f32(grad_out, "grad_out")
     out_saved = _dev_f32(out_saved, "out_saved")
-    B, L, C = path.shape
+    B, L, C = _path3(path)
     bpm, bp = _bp(basepoint, path)
     ini = None if initial is None else _dev_f32(initial, "initial")
     Lib = lib()
     S = Lib.sig_signature_channels(C, depth)
+    if S < 0:
+        raise SigError(f"bad C={C} depth={depth}")
+    M = L - 1 + (bpm != BP_NONE)
+    want = (B, M, S) if stream else (B, S)
+    _shape(grad_out, want, "grad_out")
+    _shape(out_saved, want, "out_saved")
+    if ini is not None:
+        _shape(ini, (B, S), "initial")
     gp = torch.empty_like(path)
     gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
     gi = torch.empty((B, S), device=path.device, dtype=torch.float32) if want_grad_initial else None
@@ -242,25 +286,39 @@ def sig_signature_fwd_bwd_host(path_h, grad_out_h, depth: int, chunks: int = 4, 
     return out
 
 
+@_on_device
 def sig_signature_combine(a, b, C: int, depth: int):
     a, b = _dev_f32(a, "a"), _dev_f32(b, "b")
+    S = sig_signature_channels(C, depth)
+    if a.dim() != 2 or a.shape[1] != S:
+        raise SigError(f"a must be [B, {S}], got {list(a.shape)}")
+    _shape(b, tuple(a.shape), "b")
     out = torch.empty_like(a)
     _check(lib().sig_signature_combine(_ptr(a), _ptr(b), a.shape[0], C, depth, _ptr(out), _stream(a.device)),
            "sig_signature_combine")
     return out
 
 
+@_on_device
 def sig_signature_combine_backward(grad_out, a, b, C: int, depth: int):
     grad_out, a, b = _dev_f32(grad_out, "grad_out"), _dev_f32(a, "a"), _dev_f32(b, "b")
+    S = sig_signature_channels(C, depth)
+    if a.dim() != 2 or a.shape[1] != S:
+        raise SigError(f"a must be [B, {S}], got {list(a.shape)}")
+    _shape(b, tuple(a.shape), "b")
+    _shape(grad_out, tuple(a.shape), "grad_out")
     ga, gb = torch.empty_like(a), torch.empty_like(b)
     _check(lib().sig_signature_combine_backward(_ptr(grad_out), _ptr(a), _ptr(b), a.shape[0], C, depth, _ptr(ga),
                                                 _ptr(gb), _stream(a.device)), "sig_signature_combine_backward")
     return ga, gb
 
 
+@_on_device
 def sig_multi_signature_combine(sigs, C: int, depth: int):
     """sigs [n, B, S] in time order -> [B, S]."""
     sigs = _dev_f32(sigs, "sigs")
+    if sigs.dim() != 3 or sigs.shape[2] != sig_signature_channels(C, depth):
+        raise SigError(f"sigs must be [n, B, {sig_signature_channels(C, depth)}], got {list(sigs.shape)}")
     n, B, S = sigs.shape
     Lib = lib()
     out = torch.empty((B, S), device=sigs.device, dtype=torch.float32)
@@ -299,10 +357,11 @@ class LogSigPlan:
         return cls._cache[key]
 
 
+@_on_device
 def sig_logsignature(path, depth: int, mode: str = "words", stream: bool = False, basepoint=None,
                      return_signature: bool = False):
     path = _dev_f32(path, "path")
-    B, L, C = path.shape
+    B, L, C = _path3(path)
     plan = LogSigPlan.get(C, depth, mode, path.device)
     bpm, bp = _bp(basepoint, path)
     Lib = lib()
@@ -317,15 +376,20 @@ def sig_logsignature(path, depth: int, mode: str = "words", stream: bool = False
     return (out, sig) if return_signature else out
 
 
+@_on_device
 def sig_logsignature_backward(grad_out, path, sig_saved, depth: int, mode: str = "words", stream: bool = False,
                               basepoint=None):
     path = _dev_f32(path, "path")
     grad_out = _dev_f32(grad_out, "grad_out")
     sig_saved = _dev_f32(sig_saved, "sig_saved")
-    B, L, C = path.shape
+    B, L, C = _path3(path)
     plan = LogSigPlan.get(C, depth, mode, path.device)
     bpm, bp = _bp(basepoint, path)
     Lib = lib()
+    M = L - 1 + (bpm != BP_NONE)
+    S = sig_signature_channels(C, depth)
+    _shape(grad_out, (B, M, plan.width) if stream else (B, plan.width), "grad_out")
+    _shape(sig_saved, (B, M, S) if stream else (B, S), "sig_saved")
     gp = torch.empty_like(path)
     gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
     wsb = Lib.sig_logsignature_workspace_size(plan.handle, B, L, int(stream), bpm)
@@ -437,9 +501,12 @@ def multi_signature_combine(sigs, C: int, depth: int) -> torch.Tensor:
 # ------------------------------------------------------------------------------------------------
 # logsignature of given signatures, and Path
 # ------------------------------------------------------------------------------------------------
+@_on_device
 def sig_logsignature_from_signature(sig, C: int, depth: int, mode: str = "words"):
     sig = _dev_f32(sig, "sig")
     S = sig_signature_channels(C, depth)
+    if sig.shape[-1] != S:
+        raise SigError(f"sig must be [..., {S}], got {list(sig.shape)}")
     rows = sig.numel() // S
     plan = LogSigPlan.get(C, depth, mode, sig.device)
     out = torch.empty(tuple(sig.shape[:-1]) + (plan.width,), device=sig.device, dtype=torch.float32)
@@ -448,10 +515,14 @@ def sig_logsignature_from_signature(sig, C: int, depth: int, mode: str = "words"
     return out
 
 
+@_on_device
 def sig_logsignature_from_signature_backward(grad_out, sig, C: int, depth: int, mode: str = "words"):
     sig = _dev_f32(sig, "sig")
     grad_out = _dev_f32(grad_out, "grad_out")
     S = sig_signature_channels(C, depth)
+    if sig.shape[-1] != S:
+        raise SigError(f"sig must be [..., {S}], got {list(sig.shape)}")
+    _shape(grad_out, tuple(sig.shape[:-1]) + (sig_logsignature_channels(C, depth, mode),), "grad_out")
     rows = sig.numel() // S
     plan = LogSigPlan.get(C, depth, mode, sig.device)
     Lib = lib()
@@ -491,9 +562,13 @@ def _queries(starts, ends):
     return qs, qe
 
 
+@_on_device
 def sig_path_query(prefix_sig, prefix_inv, C: int, depth: int, starts, ends):
     prefix_sig = _dev_f32(prefix_sig, "prefix_sig")
     prefix_inv = _dev_f32(prefix_inv, "prefix_inv")
+    if prefix_sig.dim() != 3 or prefix_sig.shape[2] != sig_signature_channels(C, depth):
+        raise SigError(f"prefix_sig must be [B, M, {sig_signature_channels(C, depth)}], got {list(prefix_sig.shape)}")
+    _shape(prefix_inv, tuple(prefix_sig.shape), "prefix_inv")
     B, M, S = prefix_sig.shape
     qs, qe = _queries(starts, ends)
     Q = qs.shape[0]
@@ -507,13 +582,18 @@ def sig_path_query(prefix_sig, prefix_inv, C: int, depth: int, starts, ends):
     return out
 
 
+@_on_device
 def sig_path_query_backward(grad_out, prefix_sig, prefix_inv, C: int, depth: int, starts, ends):
     prefix_sig = _dev_f32(prefix_sig, "prefix_sig")
     prefix_inv = _dev_f32(prefix_inv, "prefix_inv")
     grad_out = _dev_f32(grad_out, "grad_out")
+    if prefix_sig.dim() != 3 or prefix_sig.shape[2] != sig_signature_channels(C, depth):
+        raise SigError(f"prefix_sig must be [B, M, {sig_signature_channels(C, depth)}], got {list(prefix_sig.shape)}")
+    _shape(prefix_inv, tuple(prefix_sig.shape), "prefix_inv")
     B, M, S = prefix_sig.shape
     qs, qe = _queries(starts, ends)
     Q = qs.shape[0]
+    _shape(grad_out, (B, Q, S), "grad_out")
     Lib = lib()
     gs = torch.empty_like(prefix_sig)
     gi = torch.empty_like(prefix_inv)

@@ -207,6 +207,7 @@ cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_
             gp.out = dst;
             gp.out_sj = dsj;
             gp.out_sb = dsb;
+            gp.B = B;
             if (tf) {
                 cudaError_t e = tf(gp, (unsigned)ng, (unsigned)B, st);
                 if (e != cudaSuccess) return e;
@@ -223,7 +224,7 @@ cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_
                                                      (int)smem);
                 if (e != cudaSuccess) return e;
             }
-            dim3 grid((unsigned)ng, (unsigned)B);
+            dim3 grid((unsigned)ng, (unsigned)(B < 65535 ? B : 65535));
             combine_group_kernel<<<grid, 512, smem, st>>>(gp);
             count_launch();
         } else {
@@ -232,8 +233,8 @@ cudaError_t launch_fold(const TensorDims& d, const float* in, int64_t sj, int64_
                 const float* a = cur + 2 * q * csj;
                 float* o = dst + q * dsj;
                 if (2 * q + 1 < n) {
-                    dim3 grid((unsigned)((S + 255) / 256), (unsigned)B);
-                    combine_pair_kernel<<<grid, 256, 0, st>>>(d, a, csb, a + csj, csb, o, dsb);
+                    dim3 grid((unsigned)((S + 255) / 256), (unsigned)(B < 65535 ? B : 65535));
+                    combine_pair_kernel<<<grid, 256, 0, st>>>(d, a, csb, a + csj, csb, o, dsb, B);
                     count_launch();
                 } else {
                     cudaError_t e = cudaMemcpy2DAsync(o, dsb * sizeof(float), a, csb * sizeof(float),
@@ -777,9 +778,45 @@ static size_t host_fb_layout(int64_t B, int64_t L, int64_t C, int32_t depth, int
     off[2] = o; o = align256(o + (size_t)B * S * sizeof(float));
     off[3] = o; o = align256(o + (size_t)B * L * C * sizeof(float));
     off[4] = o;
-    FwdPlan pl;
+    // the slices are bc paths each except a shorter last one, whose plan may differ (time chunks)
+    FwdPlan pl, pll;
+    const int64_t last = B - (B - 1) / bc * bc;
     if (make_fwd_plan(bc, L, C, depth, 0, SIG_BP_NONE, pl) != SIG_OK) return 0;
-    return o + align256(pl.ws_bytes);
+    if (make_fwd_plan(last, L, C, depth, 0, SIG_BP_NONE, pll) != SIG_OK) return 0;
+    return o + align256(pl.ws_bytes > pll.ws_bytes ? pl.ws_bytes : pll.ws_bytes);
+}
+
+// Copy streams and events of the host pipeline, per device and per host thread (a stream belongs to
+// the device that was current when it was created).  Events are reused call after call: every wait
+// on them is enqueued before the call returns.
+struct HostPipeRes {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev;
+};
+
+static sig_status_t host_pipe_res(int n_events, HostPipeRes*& out) {
+    thread_local std::vector<std::pair<int, HostPipeRes>> per_dev;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    HostPipeRes* r = nullptr;
+    for (auto& pr : per_dev)
+        if (pr.first == dev) r = &pr.second;
+    if (!r) {
+        per_dev.emplace_back(dev, HostPipeRes{});
+        r = &per_dev.back().second;
+    }
+    if (!r->h2d && (e = cudaStreamCreateWithFlags(&r->h2d, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_status(e, "stream");
+    if (!r->d2h && (e = cudaStreamCreateWithFlags(&r->d2h, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_status(e, "stream");
+    while ((int)r->ev.size() < n_events) {
+        cudaEvent_t ev;
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_status(e, "event");
+        r->ev.push_back(ev);
+    }
+    out = r;
+    return SIG_OK;
 }
 
 size_t sig_signature_fwd_bwd_host_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t chunks) {
@@ -806,17 +843,20 @@ sig_status_t sig_signature_fwd_bwd_host(const float* path_h, const float* grad_o
     void* d_fws = w + off[4];
     const size_t fws_bytes = need - off[4];
     const cudaStream_t cs = (cudaStream_t)s;
-    // copy streams, created once per host thread
-    thread_local cudaStream_t h2d = nullptr, d2h = nullptr;
-    if (!h2d && cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess) return cuda_status(cudaGetLastError(), "stream");
-    if (!d2h && cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess) return cuda_status(cudaGetLastError(), "stream");
     const int64_t bc = (B + chunks - 1) / chunks;
     const int n = (int)((B + bc - 1) / bc);
-    std::vector<cudaEvent_t> ev(2 * n + 2);
-    for (auto& e : ev)
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cuda_status(cudaGetLastError(), "event");
-    auto release = [&] {
-        for (auto& e : ev) cudaEventDestroy(e);  // released once pending work completes
+    HostPipeRes* res = nullptr;
+    sig_status_t rs = host_pipe_res(2 * n + 3, res);
+    if (rs != SIG_OK) return rs;
+    const cudaStream_t h2d = res->h2d, d2h = res->d2h;
+    cudaEvent_t* ev = res->ev.data();
+    // the caller's stream resumes only after every copy issued so far (also on an early error
+    // return, so that no copy into the caller's buffers outlives the call's stream order)
+    auto join = [&] {
+        cudaEventRecord(ev[2 * n + 1], d2h);
+        cudaStreamWaitEvent(cs, ev[2 * n + 1], 0);
+        cudaEventRecord(ev[2 * n + 2], h2d);
+        cudaStreamWaitEvent(cs, ev[2 * n + 2], 0);
     };
     // the copies start after everything already queued on the caller's stream
     cudaEventRecord(ev[2 * n], cs);
@@ -839,7 +879,9 @@ sig_status_t sig_signature_fwd_bwd_host(const float* path_h, const float* grad_o
             st = sig_signature_backward(d_go + a * S, d_path + a * L * C, d_sig + a * S, b - a, L, C, depth, 0,
                                         SIG_BP_NONE, nullptr, d_gp + a * L * C, nullptr, s);
         if (st != SIG_OK) {
-            release();
+            const std::string msg = g_last_error;
+            join();
+            g_last_error = msg;
             return st;
         }
         cudaEventRecord(ev[n + k], cs);
@@ -847,10 +889,7 @@ sig_status_t sig_signature_fwd_bwd_host(const float* path_h, const float* grad_o
         cudaMemcpyAsync(grad_path_h + a * L * C, d_gp + a * L * C, (size_t)(b - a) * L * C * sizeof(float),
                         cudaMemcpyDeviceToHost, d2h);
     }
-    // the caller's stream resumes after the last read-back
-    cudaEventRecord(ev[2 * n + 1], d2h);
-    cudaStreamWaitEvent(cs, ev[2 * n + 1], 0);
-    release();
+    join();
     return cuda_status(cudaGetLastError(), "host pipeline");
 }
 
@@ -863,8 +902,8 @@ sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, in
     if (B < 0) return fail(SIG_ERR_SHAPE, "B < 0");
     if (B == 0) return ok();
     const TensorDims d = make_dims((int)C, depth);
-    dim3 grid((unsigned)((S + 255) / 256), (unsigned)B);
-    combine_pair_kernel<<<grid, 256, 0, (cudaStream_t)s>>>(d, a, S, b, S, out, S);
+    dim3 grid((unsigned)((S + 255) / 256), (unsigned)(B < 65535 ? B : 65535));
+    combine_pair_kernel<<<grid, 256, 0, (cudaStream_t)s>>>(d, a, S, b, S, out, S, B);
     count_launch();
     return cuda_status(cudaGetLastError(), "combine launch");
 }
@@ -879,8 +918,8 @@ sig_status_t sig_signature_combine_backward(const float* grad_out, const float* 
     if (B < 0) return fail(SIG_ERR_SHAPE, "B < 0");
     if (B == 0 || (!grad_a && !grad_b)) return ok();
     const TensorDims d = make_dims((int)C, depth);
-    dim3 grid((unsigned)((S + 255) / 256), (unsigned)B);
-    combine_pair_bwd_kernel<<<grid, 256, 0, (cudaStream_t)s>>>(d, grad_out, a, b, grad_a, grad_b);
+    dim3 grid((unsigned)((S + 255) / 256), (unsigned)(B < 65535 ? B : 65535));
+    combine_pair_bwd_kernel<<<grid, 256, 0, (cudaStream_t)s>>>(d, grad_out, a, b, grad_a, grad_b, B);
     count_launch();
     return cuda_status(cudaGetLastError(), "combine backward launch");
 }
@@ -980,10 +1019,12 @@ size_t sig_logsignature_workspace_size(sig_logsig_plan_t plan, int64_t B, int64_
     FwdPlan pl;
     if (make_fwd_plan(B, L, plan->C, plan->N, stream, bp, pl) != SIG_OK) return 0;
     const int64_t rows = stream ? B * pl.M : B;
-    // scan workspace | signature (if the caller gives no sig_saved) | dense dL/dlog and dL/dSig
+    // scan workspace | signature (if the caller gives no sig_saved) | dense dL/dlog and dL/dSig |
+    // the reversible backward's own workspace (time chunks of long or few paths)
     size_t a = pl.ws_bytes;
     size_t b = (size_t)rows * plan->S * sizeof(float) * 3;
-    return a + b;
+    size_t c = sig_signature_backward_ex_workspace_size(B, L, plan->C, plan->N, stream, bp, 0, 0, 0);
+    return align256(a + b) + c;
 }
 
 sig_status_t sig_logsignature(sig_logsig_plan_t plan, const float* path, int64_t B, int64_t L, int32_t stream,
@@ -1028,8 +1069,10 @@ sig_status_t sig_logsignature_backward(sig_logsig_plan_t plan, const float* grad
     float* gsig = glog + (size_t)rows * plan->S;
     st = launch_logsig_bwd(plan, grad_out, sig_saved, rows, glog, gsig, (cudaStream_t)s);
     if (st != SIG_OK) return st;
-    return sig_signature_backward(gsig, path, sig_saved, B, L, plan->C, plan->N, stream, bp, basepoint, grad_path,
-                                  grad_basepoint, s);
+    const size_t off = align256(pl.ws_bytes + (size_t)rows * plan->S * sizeof(float) * 3);
+    return sig_signature_backward_ex(gsig, path, sig_saved, B, L, plan->C, plan->N, stream, bp, basepoint, 0, nullptr,
+                                     grad_path, grad_basepoint, nullptr, static_cast<char*>(ws) + off, ws_bytes - off,
+                                     s);
 }
 
 size_t sig_logsignature_from_signature_workspace_size(sig_logsig_plan_t plan, int64_t rows) {

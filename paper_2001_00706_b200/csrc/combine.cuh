@@ -63,13 +63,15 @@ __device__ __forceinline__ float mul_coef(const TensorDims& d, const float* a, c
 #ifdef SIG_DEFINE_COMBINE_KERNELS  // defined only by api.cu, the one TU that launches them
 // ---------------------------------------------------------------- pairwise, batched
 // row r: out + r*so = (a + r*sa) [x] (b + r*sb)
+// Rows are grid-strided over gridDim.y (capped at 65535 by the launcher), so any row count works.
 __global__ void combine_pair_kernel(const TensorDims d, const float* __restrict__ a, int64_t sa,
-                                    const float* __restrict__ b, int64_t sb, float* __restrict__ out, int64_t so) {
+                                    const float* __restrict__ b, int64_t sb, float* __restrict__ out, int64_t so,
+                                    int64_t rows) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t r = blockIdx.y;
     if (f >= d.S) return;
     const int k = level_of(d, f);
-    out[r * so + f] = mul_coef(d, a + r * sa, b + r * sb, k, f - d.off[k]);
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        out[r * so + f] = mul_coef(d, a + r * sa, b + r * sb, k, f - d.off[k]);
 }
 
 // ---------------------------------------------------------------- VJP of a [x] b
@@ -101,15 +103,17 @@ __device__ __forceinline__ float gb_coef(const TensorDims& d, const float* gor, 
 }
 
 __global__ void combine_pair_bwd_kernel(const TensorDims d, const float* __restrict__ go, const float* __restrict__ a,
-                                        const float* __restrict__ b, float* __restrict__ ga, float* __restrict__ gb) {
+                                        const float* __restrict__ b, float* __restrict__ ga, float* __restrict__ gb,
+                                        int64_t rows) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t r = blockIdx.y;
     if (f >= d.S) return;
     const int i = level_of(d, f);
     const int u = f - d.off[i];
-    const float* gor = go + r * d.S;
-    if (ga) ga[r * d.S + f] = ga_coef(d, gor, b + r * d.S, i, u);
-    if (gb) gb[r * d.S + f] = gb_coef(d, gor, a + r * d.S, i, u);
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const float* gor = go + r * d.S;
+        if (ga) ga[r * d.S + f] = ga_coef(d, gor, b + r * d.S, i, u);
+        if (gb) gb[r * d.S + f] = gb_coef(d, gor, a + r * d.S, i, u);
+    }
 }
 
 // ---------------------------------------------------------------- Path interval queries
@@ -265,6 +269,7 @@ struct GroupParams {
     int G;                   // group size (power of two)
     float* out;
     int64_t out_sj, out_sb;  // group result (g, b) at out + g*out_sj + b*out_sb
+    int64_t B;               // paths (grid-strided over gridDim.y, which is capped at 65535)
 };
 
 // In-place ordered binary-tree product of cnt signatures gs[0..cnt) (S floats each) held in
@@ -294,20 +299,23 @@ __device__ __forceinline__ void block_tree_combine(float* gs, int cnt, const Ten
 __global__ void combine_group_kernel(const GroupParams p) {
     extern __shared__ float gs[];  // [G][S]
     const TensorDims& d = p.d;
-    const int64_t g = blockIdx.x, b = blockIdx.y;
+    const int64_t g = blockIdx.x;
     const int64_t j0 = g * p.G;
     const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
     const int S = d.S;
-    for (int jj = 0; jj < cnt; ++jj) {
-        const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
-        float* dst = gs + jj * S;
+    for (int64_t b = blockIdx.y; b < p.B; b += gridDim.y) {
+        for (int jj = 0; jj < cnt; ++jj) {
+            const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
+            float* dst = gs + jj * S;
 #pragma unroll 4
-        for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = __ldg(src + f);
+            for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = __ldg(src + f);
+        }
+        __syncthreads();
+        block_tree_combine(gs, cnt, d);
+        float* o = p.out + g * p.out_sj + b * p.out_sb;
+        for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = gs[f];
+        __syncthreads();
     }
-    __syncthreads();
-    block_tree_combine(gs, cnt, d);
-    float* o = p.out + g * p.out_sj + b * p.out_sb;
-    for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = gs[f];
 }
 
 #endif  // SIG_DEFINE_COMBINE_KERNELS

@@ -143,6 +143,105 @@ __device__ __forceinline__ float vjp_visit(float BI, float (&G)[SH::OWN], const 
     return beta;
 }
 
+// Fused VJP walk of the two top chains K = N-1 and K = N from node (I, W), P <= I <= N-2, carrying
+// both chain values b1 = B^(N-1)_I[p.W] and b2 = B^(N)_I[p.W]; returns beta1 = beta^(N-1)_I[p.W] and
+// beta2 = beta^(N)_I[p.W] and adds both to G_I (owned levels).  Same arithmetic as two vjp_visit
+// walks, reorganised at the level-(N-2) nodes so that no horizontal add and no separate
+// "G_{N-1} += beta_{N-1}" remain:
+//   * chain N's level-(N-1) betas are accumulated straight into G_{N-1} (beta_{N-1}[Wc] =
+//     sum_c' G_N[Wc c'] z_c' is a scalar FFMA chain seeded with G_{N-1}[Wc]);
+//   * chain N-1 must read G_{N-1} before that update (chains run bottom-up), and chain N's
+//     contributions at node W need beta_{N-1} = G_new - G_old, so the node's gz terms are
+//     bs1 G_old + bs2 (G_new - G_old) = (bs1 - bs2) G_old + bs2 G_new, and
+//     sum_c beta_{N-1}[Wc] z_c = sum_c G_new[Wc] z_c - sum_c G_old[Wc] z_c.
+// Dot products over channels are scalar FFMA chains (an FFMA2 dot product needs a horizontal add,
+// which costs an FP32 pipe cycle); the rank-1 gz updates are FFMA2 on channel pairs.
+template <class SH, int I, int W, int SA>
+__device__ __forceinline__ void vjp_top2(float b1, float b2, float (&G)[SH::OWN], const float (&A)[SA],
+                                         const float (&z)[SH::C], float (&gz)[SH::C], float& beta1, float& beta2) {
+    constexpr int C = SH::C, N = SH::N;
+    constexpr float s1 = inv_int(N - 1 - I), s2 = inv_int(N - I);
+    const float bs1 = (N - 1 - I == 1) ? b1 : b1 * s1;
+    const float bs2 = b2 * s2;
+    if constexpr (I == N - 2) {
+        constexpr int o1 = SH::own_off(N - 1) + W * C;  // G_{N-1}[W c] and A_{N-1}[W c]
+        constexpr int oN = SH::own_off(N) + W * C * C;  // G_N[W c c']
+        // chain N-1 at this node, on the old G_{N-1}
+        const float d = bs1 - bs2;
+        const float2 d2 = make_float2(d, d);
+        float acc1 = 0.0f;
+        static_for<0, C / 2>([&](auto cc) {
+            constexpr int c = 2 * decltype(cc)::value;
+            const float2 g2 = __ffma2_rn(d2, make_float2(G[o1 + c], G[o1 + c + 1]), make_float2(gz[c], gz[c + 1]));
+            gz[c] = g2.x;
+            gz[c + 1] = g2.y;
+        });
+        if constexpr (C % 2 == 1) gz[C - 1] = fmaf(d, G[o1 + C - 1], gz[C - 1]);
+        static_for<0, C>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            acc1 = fmaf(G[o1 + c], z[c], acc1);
+        });
+        // chain N: the level-(N-1) chain values of the children, B_c = bs2 z_c + A_{N-1}[W c]
+        float Bc[C];
+        const float2 bs22 = make_float2(bs2, bs2);
+        static_for<0, C / 2>([&](auto cc) {
+            constexpr int c = 2 * decltype(cc)::value;
+            const float2 r = __ffma2_rn(bs22, make_float2(z[c], z[c + 1]), make_float2(A[o1 + c], A[o1 + c + 1]));
+            Bc[c] = r.x;
+            Bc[c + 1] = r.y;
+        });
+        if constexpr (C % 2 == 1) Bc[C - 1] = fmaf(bs2, z[C - 1], A[o1 + C - 1]);
+        // the top level: gz[c'] += B_c G_N[W c c'] (FFMA2 over c' pairs); G_{N-1}[W c] += sum_c' G_N[W c c'] z_c'
+        static_for<0, C>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            const float2 b2c = make_float2(Bc[c], Bc[c]);
+            static_for<0, C / 2>([&](auto qq) {
+                constexpr int q = 2 * decltype(qq)::value;
+                const float2 g2 = __ffma2_rn(b2c, make_float2(G[oN + c * C + q], G[oN + c * C + q + 1]),
+                                             make_float2(gz[q], gz[q + 1]));
+                gz[q] = g2.x;
+                gz[q + 1] = g2.y;
+            });
+            if constexpr (C % 2 == 1) gz[C - 1] = fmaf(Bc[c], G[oN + c * C + C - 1], gz[C - 1]);
+            float g = G[o1 + c];
+            static_for<0, C>([&](auto qq) {
+                constexpr int q = decltype(qq)::value;
+                g = fmaf(G[oN + c * C + q], z[q], g);
+            });
+            G[o1 + c] = g;
+        });
+        // chain N at this node, on the new G_{N-1}
+        float acc2 = -acc1;
+        static_for<0, C / 2>([&](auto cc) {
+            constexpr int c = 2 * decltype(cc)::value;
+            const float2 g2 = __ffma2_rn(bs22, make_float2(G[o1 + c], G[o1 + c + 1]), make_float2(gz[c], gz[c + 1]));
+            gz[c] = g2.x;
+            gz[c + 1] = g2.y;
+        });
+        if constexpr (C % 2 == 1) gz[C - 1] = fmaf(bs2, G[o1 + C - 1], gz[C - 1]);
+        static_for<0, C>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            acc2 = fmaf(G[o1 + c], z[c], acc2);
+        });
+        beta1 = acc1;  // s1 = 1
+        beta2 = acc2 * s2;
+    } else {
+        float acc1 = 0.0f, acc2 = 0.0f;
+        static_for<0, C>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            constexpr int o = SH::own_off(I + 1) + W * C + c;
+            float x1, x2;
+            vjp_top2<SH, I + 1, W * C + c>(fmaf(bs1, z[c], A[o]), fmaf(bs2, z[c], A[o]), G, A, z, gz, x1, x2);
+            gz[c] = fmaf(bs1, x1, fmaf(bs2, x2, gz[c]));
+            acc1 = fmaf(x1, z[c], acc1);
+            acc2 = fmaf(x2, z[c], acc2);
+        });
+        beta1 = acc1 * s1;
+        beta2 = acc2 * s2;
+    }
+    if constexpr (I >= SH::K0) G[SH::own_off(I) + W] += beta1 + beta2;
+}
+
 // Prefix chain of chain K: Bp[j] = B^(K)_j[p[:j]] for j = 1..min(K-1, P) (Bp[0] = 1).
 template <class SH, int K, int SA>
 __device__ __forceinline__ void prefix_chain_all(float (&Bp)[SH::PL1], const float (&A)[SA], const float (&low)[SH::LOWA],
@@ -519,6 +618,19 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     }
 }
 
+#ifndef SIG_BWD_TOP2
+#define SIG_BWD_TOP2 1
+#endif
+// dev-only ablations of the prefix-pair kernel (wrong results; timing attribution only)
+#ifndef SIG_ABL_NOREV
+#define SIG_ABL_NOREV 0
+#endif
+#ifndef SIG_ABL_NOTOP
+#define SIG_ABL_NOTOP 0
+#endif
+#ifndef SIG_ABL_NORED
+#define SIG_ABL_NORED 0
+#endif
 #ifndef SIG_BWD2_STAGGER
 #define SIG_BWD2_STAGGER 0
 #endif
@@ -664,7 +776,20 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const B
                 chain_low<SH, k, k - 1>(Bp, low, zp);
                 low_tail<SH, k, k>(Gh[k], Bp, zp, acc, Gh);
             });
-            static_for<P, N + 1>([&](auto kc) {
+            // level P of the low tail of chain k per prefix (betas ba, bb at level P), then one shared
+            // tail from level P-1
+            auto tail_k = [&](auto kc, const float (&Bp)[SH::PL1], float ba, float bb) {
+                constexpr int k = decltype(kc)::value;
+                constexpr float sc = inv_int(k - P + 1);
+                const float bps = Bp[P - 1] * sc;
+                acc[P] = fmaf(bps, ba, acc[P]);
+                accPb = fmaf(bps, bb, accPb);
+                const float b1 = fmaf(ba * zp[P - 1], sc, (bb * zpb) * sc);
+                Gh[P - 1] += b1;
+                low_tail<SH, k, P - 1>(b1, Bp, zp, acc, Gh);
+            };
+            constexpr bool TOP2 = SIG_BWD_TOP2 && (N - 2 >= P);
+            static_for<P, (TOP2 ? N - 1 : N + 1)>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
                 constexpr float sc = inv_int(k - P + 1);
                 float Bp[SH::PL1];
@@ -678,14 +803,23 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const B
                     ba = vjp_visit<SH, k, P, 0>(fmaf(bs, zp[P - 1], Aa[SH::own_off(P)]), Ga, Aa, z, gz);
                     bb = vjp_visit<SH, k, P, 0>(fmaf(bs, zpb, Ab[SH::own_off(P)]), Gb, Ab, z, gz);
                 }
-                // level P of the low tail per prefix, then one shared tail from level P-1
-                const float bps = Bp[P - 1] * sc;
-                acc[P] = fmaf(bps, ba, acc[P]);
-                accPb = fmaf(bps, bb, accPb);
-                const float b1 = fmaf(ba * zp[P - 1], sc, (bb * zpb) * sc);
-                Gh[P - 1] += b1;
-                low_tail<SH, k, P - 1>(b1, Bp, zp, acc, Gh);
+                tail_k(kc, Bp, ba, bb);
             });
+            if constexpr (TOP2) {
+                // chains N-1 and N walked together (vjp_top2)
+                constexpr float sc1 = inv_int(N - 1 - P + 1), sc2 = inv_int(N - P + 1);
+                float Bp1[SH::PL1], Bp2[SH::PL1];
+                chain_low<SH, N - 1, P - 1>(Bp1, low, zp);
+                chain_low<SH, N, P - 1>(Bp2, low, zp);
+                const float bs1 = Bp1[P - 1] * sc1, bs2 = Bp2[P - 1] * sc2;
+                float b1a, b2a, b1b, b2b;
+                vjp_top2<SH, P, 0>(fmaf(bs1, zp[P - 1], Aa[SH::own_off(P)]), fmaf(bs2, zp[P - 1], Aa[SH::own_off(P)]),
+                                   Ga, Aa, z, gz, b1a, b2a);
+                vjp_top2<SH, P, 0>(fmaf(bs1, zpb, Ab[SH::own_off(P)]), fmaf(bs2, zpb, Ab[SH::own_off(P)]), Gb, Ab, z,
+                                   gz, b1b, b2b);
+                tail_k(std::integral_constant<int, N - 1>{}, Bp1, b1a, b1b);
+                tail_k(std::integral_constant<int, N>{}, Bp2, b2a, b2b);
+            }
 
             // ---- per-step gz: warp reduction into the tile
             float v[C];
@@ -759,8 +893,304 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const B
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K2 with the two sibling prefixes as the two lanes of every FFMA2 ("prefix-pair" layout).
+// Same algorithm and launch geometry as sig_bwd2_kernel, for shapes whose two top chains meet at the
+// prefix level (N - 2 == P, e.g. c2's (8, 5, 3)).  Everything at levels >= P is computed for both
+// prefixes at once: the state is held as float2 pairs (A[pa.w], A[pb.w]), z enters as a broadcast
+// scalar, and every dot product over channels accumulates a pair -- so there is no horizontal add
+// anywhere above P, and the instruction stream above P is pure FFMA2 (a mix of FFMA and FFMA2 runs
+// measurably slower at two warps per SM sub-partition, K2).  gz then holds one partial
+// per prefix, summed once per step.  The two top chains are walked together as in vjp_top2.
+// ---------------------------------------------------------------------------------------------
+template <class SH>
+struct BwdLayout2P {
+    static constexpr bool OK = BwdLayout2<SH>::OK && (SH::N - 2 == SH::P);
+};
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+// reversal Horner walk in pair layout: node (I, W) with BI = (B_I[pa.W], B_I[pb.W]); children
+// B_{I+1}[p.W.c] = B_I[p.W] (-z_c) / (K-I) + A_{I+1}[p.W.c]; at I+1 = K A is updated in place
+template <class SH, int K, int I, int W, int SZ>
+__device__ __forceinline__ void horner_pp_neg(float2 BI, float2 (&AP)[SZ], const float (&z)[SH::C]) {
+    constexpr int C = SH::C;
+    const float2 bs = (K - I == 1) ? BI : __fmul2_rn(BI, f2(inv_int(K - I)));
+    static_for<0, C>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        constexpr int o = SH::own_off(I + 1) + W * C + c;
+        const float2 r = __ffma2_rn(bs, f2(-z[c]), AP[o]);
+        if constexpr (I + 1 == K) AP[o] = r;
+        else horner_pp_neg<SH, K, I + 1, W * C + c>(r, AP, z);
+    });
+}
+
+template <class SH>
+__global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const BwdParams prm) {
+    using LY = BwdLayout2<SH>;
+    constexpr int C = SH::C, N = SH::N, P = SH::P;
+    static_assert(N - 2 == P && P >= 2 && C % 2 == 0, "prefix-pair K2: the top chains meet at level P");
+    constexpr int HW = LY::HW;
+    constexpr int NA = SH::OWNA;  // owned levels P..N-1
+    constexpr int NG = SH::OWN;   // owned levels P..N
+    extern __shared__ __align__(16) float sm[];
+    const int64_t bidx = blockIdx.x;
+    const int64_t M = prm.M;
+    const int T = LY::tile(M);
+    float* zbuf = sm;                                 // [M][C] increments
+    float* part = zbuf + (M * C + 3) / 4 * 4;         // [T][HW][C] per-warp gz records
+    float* tot = part + (size_t)T * HW * C;           // [T][C] per-step gz totals
+    float* gprev = tot + (size_t)T * C;               // [C]
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int has_bp = prm.bp_mode != 0;
+    const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;
+    const float* gorow = prm.grad_out + (size_t)bidx * prm.go_stride;
+
+    for (int64_t e = tid; e < M * C; e += blockDim.x) {
+        const int64_t s = e / C;
+        const int c = (int)(e % C);
+        const float* xr = prm.path + bidx * prm.L * C;
+        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
+        const float x1 = xr[r1 * C + c];
+        const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
+        zbuf[e] = prm.zsign * (x1 - x0);
+    }
+    if (tid < C) gprev[tid] = 0.0f;
+
+    const int pa = 2 * tid;  // prefixes pa, pa + 1: same p[:P-1], last digits p[P-1], p[P-1] + 1
+    int p[SH::PD];
+    prefix_digits<SH>(pa, p);
+    float2 AP[NA], GP[NG];
+    float low[SH::LOWA], Gh[SH::LOWA];
+    static_for<SH::K0, N + 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        constexpr int n = SH::own(k);
+        float ta[n], tb[n];
+        if constexpr (k < N) {
+            load_run<n, 0>(ta, sigrow + SH::lvl_off(k) + (int64_t)pa * n);
+            load_run<n, 0>(tb, sigrow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
+#pragma unroll
+            for (int q = 0; q < n; ++q) AP[SH::own_off(k) + q] = make_float2(ta[q], tb[q]);
+        }
+        load_run<n, 0>(ta, gorow + SH::lvl_off(k) + (int64_t)pa * n);
+        load_run<n, 0>(tb, gorow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
+#pragma unroll
+        for (int q = 0; q < n; ++q) GP[SH::own_off(k) + q] = make_float2(ta[q], tb[q]);
+    });
+    low[0] = 0.0f;
+    Gh[0] = 0.0f;
+    static_for<1, P>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        constexpr int tail = (int)ipow(C, P - i);
+        low[i] = sigrow[SH::lvl_off(i) + pa / tail];
+        Gh[i] = (pa % tail == 0) ? gorow[SH::lvl_off(i) + pa / tail] : 0.0f;
+    });
+    __syncthreads();
+
+    constexpr int HC = C / 2;
+    const int gbase = lane & ~(C - 1);
+    const int ch = lane & (C - 1);
+    const int chP1_g0 = ((tid & ~(C - 1)) / HC) % C;
+    const int chP1_g1 = (((tid & ~(C - 1)) + HC) / HC) % C;
+    constexpr int oP = SH::own_off(P), o1 = SH::own_off(N - 1), oN = SH::own_off(N);
+
+    for (int64_t n0 = 0; n0 < M; n0 += T) {
+        const int tn = (int)((M - n0) < T ? (M - n0) : T);
+        for (int j = 0; j < tn; ++j) {
+            const int64_t t = M - 1 - (n0 + j);
+            float z[C], zp[SH::PD];
+#pragma unroll
+            for (int c = 0; c < C; ++c) z[c] = zbuf[t * C + c];
+#pragma unroll
+            for (int q = 0; q < SH::PD; ++q) zp[q] = zbuf[t * C + p[q]];
+            const float zpb = zbuf[t * C + p[P - 1] + 1];
+            const float2 zpp = make_float2(zp[P - 1], zpb);
+            // (1) reversibility A <- A [x] exp(-z) on levels < N; the exact start state at t = 0
+            if (!SIG_ABL_NOREV && t > 0) {
+                static_for<0, N - 1 - P + 1>([&](auto kkc) {
+                    constexpr int k = N - 1 - decltype(kkc)::value;  // N-1 .. P
+                    float b = 1.0f;
+                    static_for<1, P>([&](auto ic) {
+                        constexpr int i = decltype(ic)::value;
+                        if constexpr (i == 1) b = fmaf(zp[0], -inv_int(k), low[i]);
+                        else b = fmaf(b * (-inv_int(k - i + 1)), zp[i - 1], low[i]);
+                    });
+                    const float2 BP = __ffma2_rn(f2(b * (-inv_int(k - P + 1))), zpp, AP[oP]);
+                    if constexpr (k == P) AP[oP] = BP;
+                    else horner_pp_neg<SH, k, P, 0>(BP, AP, z);
+                });
+                static_for<0, P - 1>([&](auto kkc) {
+                    constexpr int k = P - 1 - decltype(kkc)::value;
+                    float b = 1.0f;
+                    static_for<1, k + 1>([&](auto ic) {
+                        constexpr int i = decltype(ic)::value;
+                        if constexpr (i == 1) b = fmaf(zp[0], -inv_int(k), low[i]);
+                        else b = fmaf(b * (-inv_int(k - i + 1)), zp[i - 1], low[i]);
+                    });
+                    low[k] = b;
+                });
+            } else {
+#pragma unroll
+                for (int q = 0; q < NA; ++q) AP[q] = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int q = 0; q < SH::LOWA; ++q) low[q] = 0.0f;
+            }
+            // (2)+(3): chains k = 1..N bottom-up
+            float acc[SH::PL1];
+#pragma unroll
+            for (int q = 0; q < SH::PL1; ++q) acc[q] = 0.0f;
+            float accPb = 0.0f;
+            auto tail_k = [&](auto kc, const float (&Bp)[SH::PL1], float ba, float bb) {
+                constexpr int k = decltype(kc)::value;
+                constexpr float sc = inv_int(k - P + 1);
+                const float bps = Bp[P - 1] * sc;
+                acc[P] = fmaf(bps, ba, acc[P]);
+                accPb = fmaf(bps, bb, accPb);
+                const float b1 = fmaf(ba * zp[P - 1], sc, (bb * zpb) * sc);
+                Gh[P - 1] += b1;
+                low_tail<SH, k, P - 1>(b1, Bp, zp, acc, Gh);
+            };
+            static_for<1, P>([&](auto kc) {  // chains entirely below P
+                constexpr int k = decltype(kc)::value;
+                float Bp[SH::PL1];
+                chain_low<SH, k, k - 1>(Bp, low, zp);
+                low_tail<SH, k, k>(Gh[k], Bp, zp, acc, Gh);
+            });
+            {  // chain P: its leaf is G_P itself
+                float Bp[SH::PL1];
+                chain_low<SH, P, P - 1>(Bp, low, zp);
+                tail_k(std::integral_constant<int, P>{}, Bp, GP[oP].x, GP[oP].y);
+            }
+            // chains N-1 and N together (see vjp_top2), both prefixes per FFMA2
+            float2 gzab[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) gzab[c] = make_float2(0.0f, 0.0f);
+            float Bp1[SH::PL1], Bp2[SH::PL1];
+            chain_low<SH, N - 1, P - 1>(Bp1, low, zp);
+            chain_low<SH, N, P - 1>(Bp2, low, zp);
+            const float2 b1 = __ffma2_rn(f2(Bp1[P - 1] * inv_int(N - P)), zpp, AP[oP]);      // B^(N-1)_P
+            const float2 bs2 = __fmul2_rn(__ffma2_rn(f2(Bp2[P - 1] * inv_int(N - P + 1)), zpp, AP[oP]),
+                                          f2(0.5f));                                        // B^(N)_P / 2
+            const float2 d = __ffma2_rn(bs2, f2(-1.0f), b1);
+            float2 acc1 = make_float2(0.0f, 0.0f);
+            static_for<0, C>([&](auto cc) {  // chain N-1 on the old G_{N-1}
+                constexpr int c = decltype(cc)::value;
+                gzab[c] = __ffma2_rn(d, GP[o1 + c], gzab[c]);
+                acc1 = __ffma2_rn(GP[o1 + c], f2(z[c]), acc1);
+            });
+            float2 Bc[C];
+            static_for<0, C>([&](auto cc) {
+                constexpr int c = decltype(cc)::value;
+                Bc[c] = __ffma2_rn(bs2, f2(z[c]), AP[o1 + c]);
+            });
+            // the top level, in blocks of C independent accumulators sharing one operand: row k of
+            // the rank-1 gz update (B_k reused), then column k of the dot products (z_k reused)
+            if (!SIG_ABL_NOTOP) static_for<0, C>([&](auto kk) {
+                constexpr int k = decltype(kk)::value;
+                static_for<0, C>([&](auto qq) {
+                    constexpr int q = decltype(qq)::value;
+                    gzab[q] = __ffma2_rn(Bc[k], GP[oN + k * C + q], gzab[q]);
+                });
+                static_for<0, C>([&](auto cc) {
+                    constexpr int c = decltype(cc)::value;
+                    GP[o1 + c] = __ffma2_rn(GP[oN + c * C + k], f2(z[k]), GP[o1 + c]);
+                });
+            });
+            float2 acc2 = make_float2(-acc1.x, -acc1.y);
+            static_for<0, C>([&](auto cc) {  // chain N on the new G_{N-1}
+                constexpr int c = decltype(cc)::value;
+                gzab[c] = __ffma2_rn(bs2, GP[o1 + c], gzab[c]);
+                acc2 = __ffma2_rn(GP[o1 + c], f2(z[c]), acc2);
+            });
+            const float2 beta2 = __fmul2_rn(acc2, f2(0.5f));
+            GP[oP] = __fadd2_rn(GP[oP], __fadd2_rn(acc1, beta2));
+            tail_k(std::integral_constant<int, N - 1>{}, Bp1, acc1.x, acc1.y);
+            tail_k(std::integral_constant<int, N>{}, Bp2, beta2.x, beta2.y);
+
+            // ---- per-step gz: the two prefix partials, then the warp reduction into the tile
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = gzab[c].x + gzab[c].y;
+            if (SIG_ABL_NORED) {
+                float sv = accPb + acc[P] + acc[P - 1];
+#pragma unroll
+                for (int c = 0; c < C; ++c) sv += v[c];
+                if (lane < C) part[((size_t)j * HW + warp) * C + lane] = sv;
+                continue;
+            }
+            static_for<0, ilog2(C)>([&](auto sc_) {
+                constexpr int m = C >> (decltype(sc_)::value + 1);
+                const bool up = (lane & m) != 0;
+#pragma unroll
+                for (int q = 0; q < m; ++q) {
+                    const float send = up ? v[q] : v[q + m];
+                    const float keep = up ? v[q + m] : v[q];
+                    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                }
+            });
+            float tv = v[0];
+            {
+                const float u0 = acc[P] + __shfl_xor_sync(0xffffffffu, acc[P], HC);
+                const float u1 = accPb + __shfl_xor_sync(0xffffffffu, accPb, HC);
+                const float t0 = __shfl_sync(0xffffffffu, u0, gbase + (ch >> 1));
+                const float t1 = __shfl_sync(0xffffffffu, u1, gbase + (ch >> 1));
+                tv += (ch & 1) ? t1 : t0;
+            }
+            {
+                float gs = acc[P - 1];
+#pragma unroll
+                for (int m = 1; m < HC; m <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, m);
+                const float s0 = __shfl_sync(0xffffffffu, gs, gbase);
+                const float s1 = __shfl_sync(0xffffffffu, gs, gbase + HC);
+                if (ch == chP1_g0) tv += s0;
+                if (ch == chP1_g1) tv += s1;
+            }
+            static_for<1, P - 1>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                float gsum = acc[i];
+#pragma unroll
+                for (int m = 1; m < C; m <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, m);
+                if (ch == p[i - 1]) tv += gsum;
+            });
+#pragma unroll
+            for (int m = C; m < 32; m <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, m);
+            if (lane < C) part[((size_t)j * HW + warp) * C + lane] = tv;
+        }
+        // ---- flush
+        __syncthreads();
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            float s = 0.0f;
+            for (int w = 0; w < HW; ++w) s += part[((size_t)j * HW + w) * C + c];
+            tot[j * C + c] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            const int64_t t = M - 1 - (n0 + j);
+            const float before = (j == 0) ? gprev[c] : tot[(j - 1) * C + c];
+            const int64_t r = t + 1;
+            float* gr = has_bp ? prm.grad_path + (bidx * prm.L + (r - 1)) * C : prm.grad_path + (bidx * prm.L + r) * C;
+            gr[c] = prm.zsign * (tot[j * C + c] - before);
+            if (t == 0) {
+                float* g0 = has_bp ? ((prm.bp_mode == 2 && prm.grad_bp) ? prm.grad_bp + bidx * C : nullptr)
+                                   : prm.grad_path + bidx * prm.L * C;
+                if (g0) g0[c] = -prm.zsign * tot[j * C + c];
+            }
+        }
+        __syncthreads();
+        if (tid < C) gprev[tid] = tot[(tn - 1) * C + tid];
+        __syncthreads();
+    }
+}
+
 #ifndef SIG_BWD2
 #define SIG_BWD2 1
+#endif
+#ifndef SIG_BWD2P
+#define SIG_BWD2P 1
 #endif
 
 template <class SH>
@@ -770,12 +1200,13 @@ cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
         if (!prm.stream && prm.n_chunks == 1 && prm.initial == nullptr && prm.grad_initial == nullptr) {
             const size_t smem2 = LY2::smem_bytes(prm.M);
             if (smem2 <= 227 * 1024) {
+                auto kern = sig_bwd2_kernel<SH>;
+                if constexpr (SIG_BWD2P && BwdLayout2P<SH>::OK) kern = sig_bwd2p_kernel<SH>;
                 if (smem2 > 48 * 1024) {
-                    cudaError_t e = cudaFuncSetAttribute(sig_bwd2_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)smem2);
+                    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
                     if (e != cudaSuccess) return e;
                 }
-                sig_bwd2_kernel<SH><<<(unsigned)prm.B, LY2::NT, smem2, st>>>(prm);
+                kern<<<(unsigned)prm.B, LY2::NT, smem2, st>>>(prm);
                 return cudaGetLastError();
             }
         }

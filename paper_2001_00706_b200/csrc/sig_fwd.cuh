@@ -257,18 +257,21 @@ template <class SH>
 __global__ void __launch_bounds__(512) fold_group_t_kernel(const GroupParams p) {
     extern __shared__ __align__(16) float gs[];  // [G][S] + [ceil(G/2)][S]
     constexpr int S = (int)SH::S;
-    const int64_t g = blockIdx.x, b = blockIdx.y;
+    const int64_t g = blockIdx.x;
     const int64_t j0 = g * p.G;
     const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
-    for (int jj = 0; jj < cnt; ++jj) {
-        const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
-        float* dst = gs + (size_t)jj * S;
-        for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = __ldg(src + f);
+    for (int64_t b = blockIdx.y; b < p.B; b += gridDim.y) {  // gridDim.y is capped at 65535
+        for (int jj = 0; jj < cnt; ++jj) {
+            const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
+            float* dst = gs + (size_t)jj * S;
+            for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = __ldg(src + f);
+        }
+        __syncthreads();
+        const float* prod = block_fold_t<SH>(gs, gs + (size_t)p.G * S, cnt);
+        float* o = p.out + g * p.out_sj + b * p.out_sb;
+        for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = prod[f];
+        __syncthreads();
     }
-    __syncthreads();
-    const float* prod = block_fold_t<SH>(gs, gs + (size_t)p.G * S, cnt);
-    float* o = p.out + g * p.out_sj + b * p.out_sb;
-    for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = prod[f];
 }
 
 template <class SH>
@@ -279,7 +282,7 @@ cudaError_t launch_fold_group_t(const GroupParams& p, unsigned ngroups, unsigned
         cudaError_t e = cudaFuncSetAttribute(fold_group_t_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    fold_group_t_kernel<SH><<<dim3(ngroups, B), 512, smem, st>>>(p);
+    fold_group_t_kernel<SH><<<dim3(ngroups, B < 65535u ? B : 65535u), 512, smem, st>>>(p);
     return cudaGetLastError();
 }
 

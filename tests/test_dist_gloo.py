@@ -33,16 +33,30 @@ def _oracle_fold(sigs, C, depth):
     return torch.from_numpy(oracle.multi_combine(sigs.numpy(), C, depth))
 
 
+def _oracle_combine_bwd(g, a, b, C, depth):
+    return torch.from_numpy(np.stack([oracle.mul_vjp(g[i].numpy(), a[i].numpy(), b[i].numpy(), C, depth)[0]
+                                      for i in range(g.shape[0])]))
+
+
+def _oracle_local_bwd(g, x, out, depth, initial):
+    gx, _, _ = oracle.signature_vjp_ex(g.numpy(), x.numpy(), depth,
+                                       initial=None if initial is None else initial.numpy())
+    return torch.from_numpy(gx)
+
+
 def _work(rank, world, L, C, N):
     x = brownian_paths(2, L, C, seed=42)
     a, b = sdist.time_chunk_bounds(L, world, rank)
     xl = torch.from_numpy(x[:, a:b].astype(np.float64))
-    sig = sdist.dist_signature_timechunk(xl, N, local_sig=_oracle_sig, fold=_oracle_fold)
+    sig, parts = sdist.dist_signature_timechunk(xl, N, local_sig=_oracle_sig, fold=_oracle_fold, return_parts=True)
+    gsig = torch.from_numpy(np.random.default_rng(3).standard_normal(sig.shape))
+    gx = sdist.dist_signature_timechunk_backward(gsig, xl, parts, N, fold=_oracle_fold,
+                                                 combine_bwd=_oracle_combine_bwd, local_bwd=_oracle_local_bwd)
     # batch sharding: each rank its own slice, no collective
     lo, hi = sdist.batch_bounds(5, world, rank)
     xb = brownian_paths(5, 9, C, seed=7)
     sb = sdist.dist_signature_batch(torch.from_numpy(xb[lo:hi].astype(np.float64)), N, local_sig=_oracle_sig)
-    return rank, sig.numpy(), lo, hi, sb.numpy()
+    return rank, sig.numpy(), lo, hi, sb.numpy(), gx
 
 
 def _worker(rank, world, port, L, C, N, q):
@@ -52,7 +66,7 @@ def _worker(rank, world, port, L, C, N, q):
     try:
         q.put(_work(rank, world, L, C, N))
     except Exception as e:  # surface worker failures instead of hanging the parent
-        q.put((rank, repr(e), None, None, None))
+        q.put((rank, repr(e), None, None, None, None))
     finally:
         dist.destroy_process_group()
 
@@ -76,9 +90,15 @@ def test_timechunk_and_batch_world2(L):
     ref = oracle.signature(x, N)
     xb = brownian_paths(5, 9, C, seed=7)
     refb = oracle.signature(xb, N)
-    for rank, sig, lo, hi, sb in sorted(res, key=lambda r: r[0]):
+    for rank, sig, lo, hi, sb, _ in sorted(res, key=lambda r: r[0]):
         np.testing.assert_allclose(sig, ref, rtol=1e-11, atol=1e-13)  # replicated on every rank
         np.testing.assert_allclose(sb, refb[lo:hi], rtol=1e-12)
+    # time-chunked backward: the ranks' point gradients, shared points summed, equal the VJP of the
+    # whole path's signature
+    gsig = np.random.default_rng(3).standard_normal(ref.shape)
+    rg, _ = oracle.signature_vjp(gsig, x, N)
+    got = sdist.assemble_timechunk_grad([r[5] for r in sorted(res, key=lambda r: r[0])], L).numpy()
+    np.testing.assert_allclose(got, rg, rtol=1e-9, atol=1e-11)
 
 
 def test_bounds_partition_exactly():
