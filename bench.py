@@ -134,7 +134,7 @@ def cpu_baseline(cfg_name: str, seconds: float = 15.0) -> dict:
     C, N, L = cfg["C"], cfg["N"], cfg["L"]
     cores = len(os.sched_getaffinity(0)) or 1
     ps, gs = SEEDS[cfg_name]
-    if cfg_name == "c5":
+    if cfg_name in ("c5", "c5b"):
         Ls = 2 ** 17 + 1
         x = brownian_paths(1, L, C, ps)[:, :Ls]
         t0 = time.perf_counter()
@@ -164,7 +164,7 @@ def _oracle_step(oracle, cfg_name, x, gs, threads):
     cfg = CONFIGS[cfg_name]
     C, N = cfg["C"], cfg["N"]
     S = sum(C ** k for k in range(1, N + 1))
-    if cfg["op"] == "sig_fwd_bwd":
+    if cfg["op"] in ("sig_fwd_bwd", "sig_fwd_bwd_timechunk"):
         g = normal((x.shape[0], S), gs)
         oracle.signature_vjp(g, x, N, threads=threads)  # includes the forward it needs
     elif cfg["op"] == "logsig_words_fwd_bwd":
@@ -184,7 +184,7 @@ def run_reference(args, rank: int, world: int):
     import oracle
 
     cores = len(os.sched_getaffinity(0)) or 1
-    if args.config == "c5":  # one long path: each step is a bounded prefix, scaled to whole paths
+    if args.config in ("c5", "c5b"):  # one long path: each step is a bounded prefix, scaled to whole paths
         Ls = 2 ** 16 + 1
         x = brownian_paths(1, cfg["L"], cfg["C"], SEEDS["c5"][0])[:, :Ls]
         n = (Ls - 1) / (cfg["L"] - 1)
@@ -218,7 +218,7 @@ def run_reference(args, rank: int, world: int):
 def _config_dict(name, world, scaling="weak", B=None, l2=None):
     cfg = CONFIGS[name]
     B = B or cfg["B"]
-    if name == "c5":
+    if name in ("c5", "c5b"):
         par = f"time-chunk x{world} (NCCL all-gather + ordered fold)" if world > 1 else "single GPU"
         bdesc = "B=1"
     elif scaling == "strong":
@@ -261,9 +261,9 @@ class Workload:
         self.S = sb.sig_signature_channels(self.C, self.N)
         ps, gs = SEEDS[name]
         self.world, self.rank = world, rank
-        self.scaling = "strong" if name == "c5" else scaling
+        self.scaling = "strong" if name in ("c5", "c5b") else scaling
         B0 = int(batch) if batch else cfg["B"]
-        if name == "c5":
+        if name in ("c5", "c5b"):
             full = brownian_paths(1, self.L, self.C, ps)  # the one long path, time-chunked over ranks
             a, b = sdist.time_chunk_bounds(self.L, world, rank)
             self.x_np = np.ascontiguousarray(full[:, a:b])
@@ -286,7 +286,7 @@ class Workload:
         self.x = torch.from_numpy(self.x_np).to(dev)
         self.g = None
         gseed = (gs or 0) + (7919 * rank if self.scaling == "weak" else 0)
-        if cfg["op"] == "sig_fwd_bwd":
+        if cfg["op"] in ("sig_fwd_bwd", "sig_fwd_bwd_timechunk"):
             self.g_np = normal((B0, self.S), gseed)[self.gsl]
         elif cfg["op"] == "logsig_words_fwd_bwd":
             self.g_np = normal((B0, sb.sig_logsignature_channels(self.C, self.N, "words")), gseed)[self.gsl]
@@ -306,6 +306,7 @@ class Workload:
             ws += self.B * self.S * 4 * 4
         self.working_set = ws
         self.flush = ws <= L2_BYTES
+        self.graph = name == "c1"  # latency-bound: replay the step from a CUDA graph (time_workload)
         self.l2 = (f"per-step working set {ws / 1e6:.0f} MB > 126 MB L2; no flush needed" if not self.flush else
                    f"per-step working set {ws / 1e6:.1f} MB < L2: L2 flushed (256 MB write) before every timed step, "
                    f"outside the per-step events")
@@ -336,6 +337,18 @@ class Workload:
 
             res = sdist.dist_signature_timechunk(x, N) if self.world > 1 else sb.sig_signature(x, N)
             mark("fwd")
+        elif op == "sig_fwd_bwd_timechunk":
+            from paper_2001_00706_b200 import dist as sdist
+
+            if self.world > 1:
+                sig, parts = sdist.dist_signature_timechunk(x, N, return_parts=True)
+                mark("fwd")
+                res = sdist.dist_signature_timechunk_backward(g, x, parts, N)
+            else:
+                out = sb.sig_signature(x, N)
+                mark("fwd")
+                res, _ = sb.sig_signature_backward(g, x, out, N)
+            mark("bwd")
         else:
             res = sb.sig_signature(x, N, stream=self.cfg["stream"])
             mark("fwd")
@@ -382,12 +395,15 @@ class Workload:
         except Exception:
             traffic = {}
         meas = (lambda a: {"peak_measured": peak_meas, "frac_of_measured": a / peak_meas} if peak_meas else {})
-        if op in ("sig_fwd_bwd", "logsig_words_fwd_bwd"):
+        if op in ("sig_fwd_bwd", "logsig_words_fwd_bwd", "sig_fwd_bwd_timechunk"):
             f_fwd = alg_flops("fwd", B, M, C, N)
             f_bwd = alg_flops("bwd", B, M, C, N)
             ach = f_bwd / (seg_ms["bwd"] / 1000) / 1e12
-            kern = ("sig_bwd2p_kernel (reversible backward, sibling prefixes packed per FFMA2)" if op == "sig_fwd_bwd"
-                    else "sig_logsignature_backward call = logsig_bwd_kernel + sig_bwd_kernel (sig-bwd FLOPs only)")
+            kern = {"sig_fwd_bwd": "sig_bwd2p_kernel (reversible backward, sibling prefixes packed per FFMA2)",
+                    "logsig_words_fwd_bwd": "sig_logsignature_backward call = logsig_bwd_kernel + sig_bwd_kernel "
+                                            "(sig-bwd FLOPs only)",
+                    "sig_fwd_bwd_timechunk": "time-parallel reversible backward (chunk signatures, ordered scans, "
+                                             "chunk-end VJPs, sig_bwd_kernel over all chunks)"}[op]
             r = {"bound": "alu", "kernel": kern, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                  "frac": ach / peak, "traffic": traffic.get("sig_bwd_kernel"), "peak_source": peak_src,
                  "kernel_ms": seg_ms["bwd"], "step_share": seg_ms["bwd"] / (seg_ms["fwd"] + seg_ms["bwd"]),
@@ -484,6 +500,23 @@ def time_workload(wl, steps: int, warmup: int, world: int, dev, split_every: int
     for _ in range(warmup):
         wl.step()
     torch.cuda.synchronize(dev)
+    graph = None
+    if wl.graph:
+        # latency-bound step (c1: ~10 us of GPU work behind ~20 us of Python launch overhead): the
+        # step's C-ABI calls are captured once in a CUDA graph and replayed -- the same kernels on
+        # the same inputs every step, without the host launch cost between them
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            wl.step()
+        stream.wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        c0 = sb.lib().sig_launch_count()
+        with torch.cuda.graph(graph):
+            wl.step()
+        graph_launches = sb.lib().sig_launch_count() - c0  # kernels per replayed step
+        torch.cuda.synchronize(dev)
+        split_every = 0
     _barrier(world)
     torch.cuda.synchronize(dev)
     launches0 = sb.lib().sig_launch_count()
@@ -498,7 +531,9 @@ def time_workload(wl, steps: int, warmup: int, world: int, dev, split_every: int
                 flush.zero_()  # evict the previous step's data from L2 (outside the per-step events)
             a, b = ev(), ev()
             a.record(stream)
-            if split_every and i % split_every == 0:
+            if graph is not None:
+                graph.replay()
+            elif split_every and i % split_every == 0:
                 rec = []
                 wl.step(rec)
                 splits.append(rec)
@@ -511,6 +546,8 @@ def time_workload(wl, steps: int, warmup: int, world: int, dev, split_every: int
     _barrier(world)
     torch.cuda.synchronize(dev)
     launches = sb.lib().sig_launch_count() - launches0
+    if graph is not None:
+        launches = graph_launches * steps
     per_step = [a.elapsed_time(b) for a, b in marks]
     # with flushes between steps the block time includes them: the step time is the sum of the steps
     block = sum(per_step) if flush is not None else t_start.elapsed_time(t_end)
@@ -520,7 +557,9 @@ def time_workload(wl, steps: int, warmup: int, world: int, dev, split_every: int
         for (la, ea), (lb, eb) in zip(rec, rec[1:]):
             seg.setdefault(lb, []).append(ea.elapsed_time(eb))
     seg_ms = {k: float(np.mean(v)) for k, v in seg.items()}
-    return {"ms_step": ms_step, "ms_min": _max_over_ranks(float(np.min(per_step)), world, dev),
+    if graph is not None:
+        seg_ms = {"fwd": float(np.mean(per_step))}  # one forward launch per step
+    return {"ms_step": ms_step, "graph": graph is not None, "ms_min": _max_over_ranks(float(np.min(per_step)), world, dev),
             "ms_median": _max_over_ranks(float(np.median(per_step)), world, dev), "seg_ms": seg_ms,
             "launches": int(launches)}
 
@@ -578,7 +617,8 @@ def measure_config(name, rank, world, dev, steps, warmup, scaling="weak", batch=
            "ms_per_step": r["ms_step"], "ms_min": r["ms_min"], "ms_median": r["ms_median"], "steps": steps,
            "warmup": warmup, "scaling": wl.scaling,
            "config": _config_dict(name, world, wl.scaling, wl.B_global if wl.scaling == "strong" else wl.B, wl.l2),
-           "roofline": wl.roofline(r["seg_ms"], r["ms_step"]), "gpu_launches": r["launches"]}
+           "roofline": wl.roofline(r["seg_ms"], r["ms_step"]), "gpu_launches": r["launches"],
+           "cuda_graph": r["graph"]}
     del wl
     return out
 
@@ -619,7 +659,7 @@ def run_ours(args, rank: int, world: int):
     # every other BASELINE config, bounded, in the same run (c1 is a single-GPU row)
     if not args.no_configs:
         blk = {}
-        for name in ("c1", "c2", "c3", "c4", "c5"):
+        for name in ("c1", "c2", "c3", "c4", "c5", "c5b"):
             if name == args.config or (name == "c1" and world > 1):
                 continue
             blk[name] = measure_config(name, rank, world, dev, min(args.steps, 50), args.warmup)

@@ -171,7 +171,8 @@ sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path,
 
 /* ---------------------------------------------------------------- combine (K3) */
 
-/* out[b] = a[b] [x] b[b] for b < B; all [B, S]. out must not alias a or b. */
+/* out[b] = a[b] [x] b[b] for b < B; all [B, S]. out must not alias a or b.  Any B >= 0
+ * (the batch is grid-strided; no 65535 limit). */
 sig_status_t sig_signature_combine(const float* a, const float* b, int64_t B, int64_t C, int32_t depth, float* out,
                                    sig_cuda_stream_t s);
 
@@ -191,13 +192,17 @@ sig_status_t sig_multi_signature_combine(const float* sigs, int64_t n, int64_t B
 
 /* Immutable per-(C, depth, mode) tables (Lyndon words, flat indices, exact integer inverse of
  * psi o phi for BRACKETS), uploaded to the current device at creation.  A plan may be shared by
- * threads; destroy it after the last call that uses it has completed on the device. */
+ * threads; destroy it after the last call that uses it has completed on the device.
+ * SIG_ERR_UNSUPPORTED when one row of the log does not fit one CTA's shared memory: of the
+ * instantiated (C, depth), (3, 9), (3, 10), (4, 8), (5, 7), (6, 6) and (7, 6), in every mode. */
 typedef struct sig_logsig_plan_s* sig_logsig_plan_t;
 
 sig_status_t sig_logsig_plan_create(int64_t C, int32_t depth, sig_logsig_mode_t mode, sig_logsig_plan_t* plan);
 sig_status_t sig_logsig_plan_destroy(sig_logsig_plan_t plan);
 
-/* Workspace for sig_logsignature / _backward (includes the signature scan's own workspace). */
+/* Workspace for sig_logsignature / _backward: the signature scan's own workspace, the scratch rows of
+ * the log and its VJP, and the reversible backward's time-chunk workspace (so long paths and small
+ * batches take the time-parallel backward, as sig_signature_backward_ex does with its workspace). */
 size_t sig_logsignature_workspace_size(sig_logsig_plan_t plan, int64_t B, int64_t L, int32_t stream,
                                        sig_basepoint_t bp);
 

@@ -61,6 +61,11 @@ int64_t sig_channels_checked(int64_t C, int32_t depth) {
 constexpr int64_t kTargetThreads = 148LL * 1024;  // ~2 resident waves of 512-thread CTAs
 constexpr int64_t kOneWave = 148LL * 512;          // one resident wave
 constexpr int64_t kMinChunk = 64;                 // increments per time chunk, at least
+constexpr int64_t kLatencyBoundWork = 1LL << 20;  // threads x steps below which a scan is latency-bound
+#ifndef SIG_LATENCY_CHUNK
+#define SIG_LATENCY_CHUNK 16
+#endif
+constexpr int64_t kLatencyChunk = SIG_LATENCY_CHUNK;  // steps per chunk, at least, in the one-CTA-per-path plan
 
 struct FwdPlan {
     const KernelSet* ks;
@@ -137,6 +142,29 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
         pl.launch = ks->fwd1;
     }
     pl.upc = 0;
+    // Latency-bound problems (a few short paths, e.g. BASELINE config c1): one CTA per path holds
+    // K consecutive time chunks of it (the wider prefix variant), scans them concurrently and folds
+    // them in order in shared memory -- the path's signature in one launch, with a critical path of
+    // M/K steps plus log2(K) fold levels instead of M steps.
+    if (!stream && B > 0 && B <= 148 && ks->fwd1 && B * cp0 * M < kLatencyBoundWork && M >= 16) {
+        const int cp1 = (int)sigb200::ipow(C, ks->pf1);
+        int K = cp1 <= 512 ? 512 / cp1 : 0;
+        if (K > 32) K = 32;
+        if ((int64_t)K > M / kLatencyChunk) K = (int)(M / kLatencyChunk);
+        while (K >= 2 && (size_t)(K + (K + 1) / 2) * S * sizeof(float) > 200 * 1024) --K;
+        if (K >= 2) {
+            pl.P = ks->pf1;
+            pl.launch = ks->fwd1;
+            pl.upc = K;
+            pl.n_chunks = K;
+            pl.chunk_len = (M + K - 1) / K;
+            pl.n_parts = 1;
+            pl.n_fold = 0;
+            pl.G = 0;
+            pl.ws_bytes = 0;
+            return ok();
+        }
+    }
     if (pl.n_chunks > 1) {
         // group chunks so that each scan CTA folds upc consecutive chunks of one path itself
         const int cp = (int)sigb200::ipow(C, pl.P);
@@ -350,8 +378,16 @@ LogsigTables device_view(const sig_logsig_plan_s* pl) {
 
 constexpr size_t kMaxSmem = 227 * 1024 - 512;  // dynamic shared memory per CTA (static arrays need the rest)
 
+// K4's shared memory for one row: the compiled kernel where (C, N) has one (it keeps x only on
+// levels < N, so e.g. brackets at C = 8, N = 5 fit), else the generic one.
+size_t logsig_fwd_smem_any(const LDims& d, int64_t w, bool brackets) {
+    if (find_logsig_fwd_t(d.C, d.N)) return logsig_fwd_t_smem(d.C, d.N, (int)w, brackets);
+    return logsig_fwd_smem(d, (int)w, brackets);
+}
+
 sig_status_t check_logsig_smem(const LDims& d, int64_t w, bool brackets) {
-    if (logsig_fwd_smem(d, (int)w, brackets) > 227 * 1024 || logsig_bwd_smem(d, false) > kMaxSmem)
+    const bool bwd_ok = find_logsig_bwd_owned(d.C, d.N) != nullptr || logsig_bwd_smem(d, false) <= kMaxSmem;
+    if (logsig_fwd_smem_any(d, w, brackets) > 227 * 1024 || !bwd_ok)
         return fail(SIG_ERR_UNSUPPORTED, "logsignature of C=%d depth=%d exceeds one CTA's shared memory", d.C, d.N);
     return SIG_OK;
 }

@@ -45,6 +45,25 @@ LogsigFwdLaunch find_logsig_fwd_t(int C, int N) {
     }
 }
 
+namespace {
+template <int C, int... Ns>
+size_t fsmem(int N, int w, bool br, std::integer_sequence<int, Ns...>) {
+    size_t r = 0;
+    ((N == Ns + 1 ? (r = LogFwdT<C, Ns + 1>::smem(w, br), 0) : 0), ...);
+    return r;
+}
+}  // namespace
+
+size_t logsig_fwd_t_smem(int C, int N, int w, bool brackets) {
+    switch (C) {
+        case 1: return fsmem<1>(N, w, brackets, std::make_integer_sequence<int, 12>{});
+        case 2: return fsmem<2>(N, w, brackets, std::make_integer_sequence<int, 12>{});
+        case 4: return fsmem<4>(N, w, brackets, std::make_integer_sequence<int, 7>{});
+        case 8: return fsmem<8>(N, w, brackets, std::make_integer_sequence<int, 5>{});
+        default: return 0;
+    }
+}
+
 LogsigBwdLaunch find_logsig_bwd_owned(int C, int N) {
     switch (C) {
         case 1: return pick<1>(N, std::make_integer_sequence<int, 12>{});

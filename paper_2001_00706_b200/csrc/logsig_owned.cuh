@@ -441,6 +441,8 @@ cudaError_t launch_logsig_fwd_t(const LogsigParams& p, cudaStream_t st) {
 using LogsigFwdLaunch = cudaError_t (*)(const LogsigParams&, cudaStream_t);
 // nullptr when (C, N) has no compiled instance
 LogsigFwdLaunch find_logsig_fwd_t(int C, int N);
+// dynamic shared memory of the compiled K4 for one row (0 when there is no compiled instance)
+size_t logsig_fwd_t_smem(int C, int N, int w, bool brackets);
 
 using LogsigBwdLaunch = cudaError_t (*)(const LogsigParams&, cudaStream_t);
 // nullptr when (C, N) has no compiled instance (non power-of-two C, or too large for one CTA)

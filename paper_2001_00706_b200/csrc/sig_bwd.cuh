@@ -621,6 +621,10 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
 #ifndef SIG_BWD_TOP2
 #define SIG_BWD_TOP2 1
 #endif
+// prefix-pair K2: the top level's G_N in natural per-prefix order (1) or in pairs too (0)
+#ifndef SIG_BWD2P_NATTOP
+#define SIG_BWD2P_NATTOP 0
+#endif
 // dev-only ablations of the prefix-pair kernel (wrong results; timing attribution only)
 #ifndef SIG_ABL_NOREV
 #define SIG_ABL_NOREV 0
@@ -947,11 +951,11 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
     const int has_bp = prm.bp_mode != 0;
     const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;
     const float* gorow = prm.grad_out + (size_t)bidx * prm.go_stride;
+    const float* xr = prm.path + bidx * prm.L * C;
 
     for (int64_t e = tid; e < M * C; e += blockDim.x) {
         const int64_t s = e / C;
         const int c = (int)(e % C);
-        const float* xr = prm.path + bidx * prm.L * C;
         const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
         const float x1 = xr[r1 * C + c];
         const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
@@ -962,22 +966,32 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
     const int pa = 2 * tid;  // prefixes pa, pa + 1: same p[:P-1], last digits p[P-1], p[P-1] + 1
     int p[SH::PD];
     prefix_digits<SH>(pa, p);
+    // levels P..N-1 in pairs; the top level G_N per prefix in natural order (NT: the top loop's gz
+    // update is then an FFMA2 with a broadcast chain value, K2)
+    constexpr int CN = SH::own(N);
     float2 AP[NA], GP[NG];
+    float GNa[SIG_BWD2P_NATTOP ? CN : 1], GNb[SIG_BWD2P_NATTOP ? CN : 1];
     float low[SH::LOWA], Gh[SH::LOWA];
     static_for<SH::K0, N + 1>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
         constexpr int n = SH::own(k);
         float ta[n], tb[n];
+        auto ld = [&](float* dst, const float* src) { load_run<n, 0>(*reinterpret_cast<float(*)[n]>(dst), src); };
         if constexpr (k < N) {
-            load_run<n, 0>(ta, sigrow + SH::lvl_off(k) + (int64_t)pa * n);
-            load_run<n, 0>(tb, sigrow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
+            ld(ta, sigrow + SH::lvl_off(k) + (int64_t)pa * n);
+            ld(tb, sigrow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
 #pragma unroll
             for (int q = 0; q < n; ++q) AP[SH::own_off(k) + q] = make_float2(ta[q], tb[q]);
         }
-        load_run<n, 0>(ta, gorow + SH::lvl_off(k) + (int64_t)pa * n);
-        load_run<n, 0>(tb, gorow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
+        if constexpr (k == N && SIG_BWD2P_NATTOP) {
+            ld(GNa, gorow + SH::lvl_off(k) + (int64_t)pa * n);
+            ld(GNb, gorow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
+        } else {
+            ld(ta, gorow + SH::lvl_off(k) + (int64_t)pa * n);
+            ld(tb, gorow + SH::lvl_off(k) + (int64_t)(pa + 1) * n);
 #pragma unroll
-        for (int q = 0; q < n; ++q) GP[SH::own_off(k) + q] = make_float2(ta[q], tb[q]);
+            for (int q = 0; q < n; ++q) GP[SH::own_off(k) + q] = make_float2(ta[q], tb[q]);
+        }
     });
     low[0] = 0.0f;
     Gh[0] = 0.0f;
@@ -1064,9 +1078,6 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
                 tail_k(std::integral_constant<int, P>{}, Bp, GP[oP].x, GP[oP].y);
             }
             // chains N-1 and N together (see vjp_top2), both prefixes per FFMA2
-            float2 gzab[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c) gzab[c] = make_float2(0.0f, 0.0f);
             float Bp1[SH::PL1], Bp2[SH::PL1];
             chain_low<SH, N - 1, P - 1>(Bp1, low, zp);
             chain_low<SH, N, P - 1>(Bp2, low, zp);
@@ -1075,33 +1086,76 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
                                           f2(0.5f));                                        // B^(N)_P / 2
             const float2 d = __ffma2_rn(bs2, f2(-1.0f), b1);
             float2 acc1 = make_float2(0.0f, 0.0f);
-            static_for<0, C>([&](auto cc) {  // chain N-1 on the old G_{N-1}
-                constexpr int c = decltype(cc)::value;
-                gzab[c] = __ffma2_rn(d, GP[o1 + c], gzab[c]);
-                acc1 = __ffma2_rn(GP[o1 + c], f2(z[c]), acc1);
-            });
             float2 Bc[C];
             static_for<0, C>([&](auto cc) {
                 constexpr int c = decltype(cc)::value;
                 Bc[c] = __ffma2_rn(bs2, f2(z[c]), AP[o1 + c]);
             });
-            // the top level, in blocks of C independent accumulators sharing one operand: row k of
-            // the rank-1 gz update (B_k reused), then column k of the dot products (z_k reused)
-            if (!SIG_ABL_NOTOP) static_for<0, C>([&](auto kk) {
-                constexpr int k = decltype(kk)::value;
-                static_for<0, C>([&](auto qq) {
-                    constexpr int q = decltype(qq)::value;
-                    gzab[q] = __ffma2_rn(Bc[k], GP[oN + k * C + q], gzab[q]);
-                });
-                static_for<0, C>([&](auto cc) {
+            float v[C];
+            if constexpr (SIG_BWD2P_NATTOP) {
+                float gza[C], gzb[C];  // per-prefix gz partials, natural channel pairs
+                static_for<0, C>([&](auto cc) {  // chain N-1 on the old G_{N-1}
                     constexpr int c = decltype(cc)::value;
-                    GP[o1 + c] = __ffma2_rn(GP[oN + c * C + k], f2(z[k]), GP[o1 + c]);
+                    gza[c] = d.x * GP[o1 + c].x;
+                    gzb[c] = d.y * GP[o1 + c].y;
+                    acc1 = __ffma2_rn(GP[o1 + c], f2(z[c]), acc1);
                 });
-            });
+                if (!SIG_ABL_NOTOP) static_for<0, C>([&](auto cc) {  // the top level
+                    constexpr int c = decltype(cc)::value;
+                    static_for<0, C / 2>([&](auto qq) {
+                        constexpr int q = 2 * decltype(qq)::value;
+                        const float2 ra = __ffma2_rn(f2(Bc[c].x), make_float2(GNa[c * C + q], GNa[c * C + q + 1]),
+                                                     make_float2(gza[q], gza[q + 1]));
+                        gza[q] = ra.x;
+                        gza[q + 1] = ra.y;
+                        const float2 rb = __ffma2_rn(f2(Bc[c].y), make_float2(GNb[c * C + q], GNb[c * C + q + 1]),
+                                                     make_float2(gzb[q], gzb[q + 1]));
+                        gzb[q] = rb.x;
+                        gzb[q + 1] = rb.y;
+                    });
+                    float ga = GP[o1 + c].x, gb = GP[o1 + c].y;
+                    static_for<0, C>([&](auto qq) {
+                        constexpr int q = decltype(qq)::value;
+                        ga = fmaf(GNa[c * C + q], z[q], ga);
+                        gb = fmaf(GNb[c * C + q], z[q], gb);
+                    });
+                    GP[o1 + c] = make_float2(ga, gb);
+                });
+                static_for<0, C>([&](auto cc) {  // chain N on the new G_{N-1}
+                    constexpr int c = decltype(cc)::value;
+                    gza[c] = fmaf(bs2.x, GP[o1 + c].x, gza[c]);
+                    gzb[c] = fmaf(bs2.y, GP[o1 + c].y, gzb[c]);
+                    v[c] = gza[c] + gzb[c];
+                });
+            } else {
+                float2 gzab[C];
+                static_for<0, C>([&](auto cc) {  // chain N-1 on the old G_{N-1}
+                    constexpr int c = decltype(cc)::value;
+                    gzab[c] = __fmul2_rn(d, GP[o1 + c]);
+                    acc1 = __ffma2_rn(GP[o1 + c], f2(z[c]), acc1);
+                });
+                // the top level, in blocks of C independent accumulators sharing one operand: row k of
+                // the rank-1 gz update (B_k reused), then column k of the dot products (z_k reused)
+                if (!SIG_ABL_NOTOP) static_for<0, C>([&](auto kk) {
+                    constexpr int k = decltype(kk)::value;
+                    static_for<0, C>([&](auto qq) {
+                        constexpr int q = decltype(qq)::value;
+                        gzab[q] = __ffma2_rn(Bc[k], GP[oN + k * C + q], gzab[q]);
+                    });
+                    static_for<0, C>([&](auto cc) {
+                        constexpr int c = decltype(cc)::value;
+                        GP[o1 + c] = __ffma2_rn(GP[oN + c * C + k], f2(z[k]), GP[o1 + c]);
+                    });
+                });
+                static_for<0, C>([&](auto cc) {  // chain N on the new G_{N-1}
+                    constexpr int c = decltype(cc)::value;
+                    gzab[c] = __ffma2_rn(bs2, GP[o1 + c], gzab[c]);
+                    v[c] = gzab[c].x + gzab[c].y;
+                });
+            }
             float2 acc2 = make_float2(-acc1.x, -acc1.y);
-            static_for<0, C>([&](auto cc) {  // chain N on the new G_{N-1}
+            static_for<0, C>([&](auto cc) {
                 constexpr int c = decltype(cc)::value;
-                gzab[c] = __ffma2_rn(bs2, GP[o1 + c], gzab[c]);
                 acc2 = __ffma2_rn(GP[o1 + c], f2(z[c]), acc2);
             });
             const float2 beta2 = __fmul2_rn(acc2, f2(0.5f));
@@ -1109,10 +1163,7 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
             tail_k(std::integral_constant<int, N - 1>{}, Bp1, acc1.x, acc1.y);
             tail_k(std::integral_constant<int, N>{}, Bp2, beta2.x, beta2.y);
 
-            // ---- per-step gz: the two prefix partials, then the warp reduction into the tile
-            float v[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c) v[c] = gzab[c].x + gzab[c].y;
+            // ---- per-step gz (the two prefix partials were summed into v): warp reduction into the tile
             if (SIG_ABL_NORED) {
                 float sv = accPb + acc[P] + acc[P - 1];
 #pragma unroll
@@ -1201,12 +1252,14 @@ cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
             const size_t smem2 = LY2::smem_bytes(prm.M);
             if (smem2 <= 227 * 1024) {
                 auto kern = sig_bwd2_kernel<SH>;
+                size_t smem = smem2;
+                unsigned grid = (unsigned)prm.B;
                 if constexpr (SIG_BWD2P && BwdLayout2P<SH>::OK) kern = sig_bwd2p_kernel<SH>;
-                if (smem2 > 48 * 1024) {
-                    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+                if (smem > 48 * 1024) {
+                    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     if (e != cudaSuccess) return e;
                 }
-                kern<<<(unsigned)prm.B, LY2::NT, smem2, st>>>(prm);
+                kern<<<grid, LY2::NT, smem, st>>>(prm);
                 return cudaGetLastError();
             }
         }

@@ -158,6 +158,24 @@ __device__ __forceinline__ void load_run(float (&dst)[SZ], const float* src) {
     for (int i = 0; i < n; ++i) dst[OFF + i] = __ldg(src + i);
 }
 
+// Load n floats from SHARED memory src into dst[OFF .. OFF+n) (plain vector loads by alignment).
+template <int n, int OFF, int SZ>
+__device__ __forceinline__ void load_run_s(float (&dst)[SZ], const float* src) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    if constexpr (n % 4 == 0) {
+        if ((a & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(src + i);
+                dst[OFF + i] = v.x; dst[OFF + i + 1] = v.y; dst[OFF + i + 2] = v.z; dst[OFF + i + 3] = v.w;
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) dst[OFF + i] = src[i];
+}
+
 // dst[OFF .. OFF+n) += src[0 .. n), vectorised by the alignment of src (no staging array).
 template <int n, int OFF, int SZ>
 __device__ __forceinline__ void add_run(float (&dst)[SZ], const float* src) {
@@ -184,6 +202,39 @@ __device__ __forceinline__ constexpr float inv_int(int s) {
 // shared-memory address of a generic pointer into shared memory (PTX operands of the async copies)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- TMA bulk copies global -> shared completed on an mbarrier (1-D cp.async.bulk; sizes and
+// addresses multiples of 16 bytes)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+        ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+// order this thread's earlier generic-proxy accesses of shared memory before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// bulk copy of any multiple of 16 bytes, in pieces of at most 64 KB
+__device__ __forceinline__ void bulk_g2s_big(void* sdst, const void* gsrc, size_t bytes, uint64_t* bar) {
+    char* d = static_cast<char*>(sdst);
+    const char* g = static_cast<const char*>(gsrc);
+    while (bytes > 0) {
+        const unsigned n = bytes > 65536 ? 65536u : (unsigned)bytes;
+        bulk_g2s(d, g, n, bar);
+        d += n;
+        g += n;
+        bytes -= n;
+    }
 }
 
 }  // namespace sigb200

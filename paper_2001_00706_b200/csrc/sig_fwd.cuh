@@ -25,6 +25,9 @@
 #ifndef SIG_FWD_TILE_KB
 #define SIG_FWD_TILE_KB 160
 #endif
+#ifndef SIG_FWD_TMA_STAGE
+#define SIG_FWD_TMA_STAGE 1
+#endif
 
 namespace sigb200 {
 
@@ -45,6 +48,16 @@ struct FwdParams {
     float* out;              // stream: [B, M, S]; upc = 0: unit u -> out + u * S
     float zsign;             // +1, or -1: scan the negated path (the inverse option, R18)
     const float* initial;    // [B, S] start state of each path's first chunk, or nullptr (identity)
+    int64_t raw_off;         // > 0: sig_fwd_kernel stages each tile's points by TMA bulk copies into the
+                             // shared area at this float offset (nu * RawLayout::unit(tile, C) floats)
+};
+
+// TMA staging of path points (sig_fwd_kernel): a unit's tile needs the rows r0 .. r0 + cnt of its
+// path (r0 = -1 is the basepoint); the 16-byte-aligned cover of those rows is bulk-copied into a
+// per-unit slot, and the increments are formed from shared memory.  One copy and one barrier wait
+// per unit and tile, instead of several dependent rounds of global loads (c1 is latency-bound).
+struct RawLayout {
+    __host__ __device__ static int64_t unit(int tile, int C) { return (((int64_t)tile + 1) * C + 8 + 3) / 4 * 4; }
 };
 
 // Depth-first walk of the thread's word tree for the level-K Horner chain (eq-fusedterm):
@@ -318,8 +331,81 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     // the update case: the path's first chunk starts from the given signature
     if (prm.initial != nullptr && valid && j == 0) load_state<SH>(prm.initial + (size_t)b * SH::S, prefix, own, low);
 
+    __shared__ uint64_t stage_bar;
+    unsigned stage_phase = 0;
+    if (prm.raw_off > 0 && threadIdx.x == 0) mbar_init(&stage_bar, 1);
     for (int64_t t0 = 0; t0 < prm.chunk_len; t0 += T) {
         __syncthreads();
+        if (prm.raw_off > 0) {
+            // ---- TMA: the 16-byte-aligned cover of every unit's rows, one bulk copy per unit
+            float* raw = zs + prm.raw_off;
+            const int64_t ru = RawLayout::unit(T, C);
+            auto unit_rows = [&](int uu, int64_t& bb, int64_t& r0, int& cnt) {
+                const int64_t un = unit0 + uu;
+                cnt = 0;
+                bb = 0;
+                r0 = 0;
+                if (un < prm.n_units) {
+                    bb = un / prm.n_chunks;
+                    const int64_t jj = un - bb * prm.n_chunks;
+                    const int64_t ulen = (prm.chunk_len < prm.M - jj * prm.chunk_len ? prm.chunk_len
+                                                                                      : prm.M - jj * prm.chunk_len);
+                    cnt = (int)(ulen - t0 < T ? (ulen - t0 > 0 ? ulen - t0 : 0) : T);
+                    r0 = jj * prm.chunk_len + t0 - has_bp;  // point of the tile's first x0 (-1: basepoint)
+                }
+            };
+            if (threadIdx.x == 0) {
+                unsigned total = 0;
+                for (int uu = 0; uu < nu; ++uu) {
+                    int64_t bb, r0;
+                    int cnt;
+                    unit_rows(uu, bb, r0, cnt);
+                    if (cnt == 0) continue;
+                    const float* lo = prm.path + (bb * prm.L + (r0 < 0 ? 0 : r0)) * C;
+                    const float* hi = prm.path + (bb * prm.L + r0 + cnt + 1) * C;
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(lo) & ~(uintptr_t)15;
+                    const uintptr_t e = (reinterpret_cast<uintptr_t>(hi) + 15) & ~(uintptr_t)15;
+                    total += (unsigned)(e - a);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&stage_bar, total);
+                for (int uu = 0; uu < nu; ++uu) {
+                    int64_t bb, r0;
+                    int cnt;
+                    unit_rows(uu, bb, r0, cnt);
+                    if (cnt == 0) continue;
+                    const float* lo = prm.path + (bb * prm.L + (r0 < 0 ? 0 : r0)) * C;
+                    const float* hi = prm.path + (bb * prm.L + r0 + cnt + 1) * C;
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(lo) & ~(uintptr_t)15;
+                    const uintptr_t e = (reinterpret_cast<uintptr_t>(hi) + 15) & ~(uintptr_t)15;
+                    bulk_g2s(raw + uu * ru, reinterpret_cast<const void*>(a), (unsigned)(e - a), &stage_bar);
+                }
+            }
+            mbar_wait(&stage_bar, stage_phase);
+            stage_phase ^= 1u;
+            for (int uu = 0; uu < nu; ++uu) {
+                int64_t bb, r0;
+                int cnt;
+                unit_rows(uu, bb, r0, cnt);
+                const float* lo = prm.path + (bb * prm.L + (r0 < 0 ? 0 : r0)) * C;
+                const int sh = (int)((reinterpret_cast<uintptr_t>(lo) & 15) >> 2);  // floats before row max(r0, 0)
+                const float* ru_base = raw + uu * ru + sh;  // point row max(r0, 0) of the unit
+                float* zu = zs + (size_t)uu * T * C;
+                for (int i = threadIdx.x; i < T * C; i += blockDim.x) {
+                    const int t = i / C, c = i - (i / C) * C;
+                    float zv = 0.0f;
+                    if (t < cnt) {
+                        const int64_t row = r0 + t;  // x0 = point row, x1 = point row + 1
+                        const int64_t rel = row - (r0 < 0 ? 0 : r0);
+                        const float x1 = ru_base[(rel + 1) * C + c];
+                        const float x0 = (row >= 0) ? ru_base[rel * C + c]
+                                                    : ((prm.bp_mode == 2) ? prm.basepoint[bb * C + c] : 0.0f);
+                        zv = prm.zsign * (x1 - x0);
+                    }
+                    zu[t * C + zswz(C, c)] = zv;
+                }
+            }
+        } else
         // ---- stage the increments z = X[s+1] - X[s] of this tile for the CTA's units.  Per unit
         // the points are one contiguous run of the path (coalesced, independent loads unrolled for
         // memory-level parallelism); index math is 32-bit inside the tile.
@@ -405,9 +491,6 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
 // global destination; the 16-byte-aligned interior goes by TMA, the <= 3 floats at each end by
 // plain stores.  Two images per unit alternate, so the copy of one tile overlaps the next tile.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
                  "r"(bytes)
@@ -678,6 +761,18 @@ cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     while (tile > 8 && (size_t)nu * tile * SH::C * 4 > tkb * 1024) tile /= 2;
     prm.tile = tile;
     size_t smem = (size_t)nu * tile * SH::C * sizeof(float);
+    // TMA staging of the points (RawLayout) after the increments, 16-byte aligned, when it fits
+    prm.raw_off = 0;
+    {
+        const int64_t ro = ((int64_t)nu * tile * SH::C + 3) / 4 * 4;
+        const size_t need = (size_t)(ro + (int64_t)nu * RawLayout::unit(tile, SH::C)) * sizeof(float);
+        // the aligned covers stay inside the path tensor when it starts and ends on 16 bytes
+        const bool aligned = (reinterpret_cast<uintptr_t>(prm.path) & 15) == 0 && (prm.B * prm.L * SH::C) % 4 == 0;
+        if (SIG_FWD_TMA_STAGE && aligned && need <= 160 * 1024) {
+            prm.raw_off = ro;
+            smem = need;
+        }
+    }
     // grouped chunks: nu unit signatures plus the fold's second buffer of ceil(nu / 2)
     if (prm.upc > 0 && (size_t)(nu + (nu + 1) / 2) * SH::S * sizeof(float) > smem)
         smem = (size_t)(nu + (nu + 1) / 2) * SH::S * sizeof(float);

@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 # Per-config seeds: path seed / grad seed.
-SEEDS = {"c1": (1, None), "c2": (2, 102), "c3": (3, None), "c4": (4, 104), "c5": (5, None)}
+SEEDS = {"c1": (1, None), "c2": (2, 102), "c3": (3, None), "c4": (4, 104), "c5": (5, None), "c5b": (5, 105)}
 
 # BASELINE.json configs
 CONFIGS = {
@@ -25,6 +25,8 @@ CONFIGS = {
     "c3": dict(B=256, L=1024, C=6, N=4, stream=True, op="sig_fwd_stream"),
     "c4": dict(B=512, L=256, C=4, N=7, stream=False, op="logsig_words_fwd_bwd"),
     "c5": dict(B=1, L=2 ** 22, C=3, N=6, stream=False, op="sig_fwd_timechunk"),
+    # not a BASELINE config: c5's path through forward + reversible backward
+    "c5b": dict(B=1, L=2 ** 22, C=3, N=6, stream=False, op="sig_fwd_bwd_timechunk"),
 }
 
 

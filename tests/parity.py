@@ -12,14 +12,34 @@ FWD_TOL = 1e-4
 BWD_TOL = 5e-4
 
 
-def _blocks_err(gpu, ref, blocks):
+FLOOR_REL = 1e-4
+
+
+def floor_engaged(ref, blocks) -> bool:
+    """True when some (row, block) reference norm is below FLOOR_REL x its row's largest block norm,
+    i.e. when _blocks_err would judge that block against the floor instead of its own norm."""
+    r = np.asarray(ref, dtype=np.float64)
+    r = r.reshape(-1, r.shape[-1])
+    norms = np.stack([np.max(np.abs(r[:, a:b]), axis=1) for a, b in blocks], axis=1)
+    return bool(np.any(norms < FLOOR_REL * np.max(norms, axis=1, keepdims=True)))
+
+
+def level_blocks(C, N):
+    blocks, off = [], 0
+    for k in range(1, N + 1):
+        blocks.append((off, off + C ** k))
+        off += C ** k
+    return blocks
+
+
+def _blocks_err(gpu, ref, blocks, strict=False):
     gpu = np.asarray(gpu, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     W = gpu.shape[-1]
     g = gpu.reshape(-1, W)
     r = ref.reshape(-1, W)
     norms = np.stack([np.max(np.abs(r[:, a:b]), axis=1) for a, b in blocks], axis=1)  # [rows, nblocks]
-    floor = 1e-4 * np.max(norms, axis=1)
+    floor = (0.0 if strict else FLOOR_REL) * np.max(norms, axis=1)
     worst = 0.0
     for j, (a, b) in enumerate(blocks):
         num = np.max(np.abs(g[:, a:b] - r[:, a:b]), axis=1)
@@ -29,12 +49,10 @@ def _blocks_err(gpu, ref, blocks):
     return worst
 
 
-def level_rel_err(gpu, ref, C, N):
-    blocks, off = [], 0
-    for k in range(1, N + 1):
-        blocks.append((off, off + C ** k))
-        off += C ** k
-    return _blocks_err(gpu, ref, blocks)
+def level_rel_err(gpu, ref, C, N, strict=False):
+    """strict: every (row, level) against its own norm (no floor) -- used where levels of one row span
+    many orders of magnitude legitimately (the first rows of stream mode)."""
+    return _blocks_err(gpu, ref, level_blocks(C, N), strict)
 
 
 def block_rel_err(gpu, ref, blocks):
