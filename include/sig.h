@@ -104,10 +104,10 @@ sig_status_t sig_signature(const float* path, int64_t B, int64_t L, int64_t C, i
  *                  reversal eq-reverse); consistency with `path` is NOT checked
  *   grad_path      [B, L, C], overwritten
  *   grad_basepoint [B, C] (bp == SIG_BP_GIVEN) or NULL; overwritten when given
- * One CTA reverses one path and stages its increments in shared memory; a path longer than that
- * (about 227 KB of increments, shape-dependent) needs the time-parallel backward and its workspace:
- * this call then returns SIG_ERR_WORKSPACE -- use sig_signature_backward_ex with
- * sig_signature_backward_ex_workspace_size(...) bytes. */
+ * One CTA reverses one path, staging its increments in shared memory tile by tile, so any path
+ * length works here (no workspace, no time chunks).  Small batches and long paths run faster
+ * through sig_signature_backward_ex with sig_signature_backward_ex_workspace_size(...) bytes of
+ * workspace: the path is then split into time chunks reversed in parallel. */
 sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
                                     int64_t L, int64_t C, int32_t depth, int32_t stream, sig_basepoint_t bp,
                                     const float* basepoint, float* grad_path, float* grad_basepoint,
@@ -156,9 +156,12 @@ sig_status_t sig_signature_ex(const float* path, int64_t B, int64_t L, int64_t C
 /* Backward of sig_signature_ex (reversible, as sig_signature_backward).
  *   grad_initial [B, S] or NULL: overwritten with the gradient w.r.t. `initial` (the scan's start
  *                state) when given
- *   ws           sig_signature_backward_ex_workspace_size(...) bytes: 0 for inverse = 0; for
- *                inverse = 1 the alpha images of grad_out, the final state, initial and
- *                grad_initial ((rows + up to 3 B) * S floats, rows = B or B*M)
+ *   ws           sig_signature_backward_ex_workspace_size(...) bytes: for inverse = 1 the alpha
+ *                images of grad_out, the final state, initial and grad_initial ((rows + up to 3 B)
+ *                * S floats, rows = B or B*M); then, when the batch alone cannot fill the GPU
+ *                (fewer paths than one resident wave of the backward), the time-chunk buffers
+ *                (5 B m S + B m C floats for m chunks).  With a smaller ws (or NULL) the call runs
+ *                without time chunks.
  * Errors as sig_signature_backward; WORKSPACE when ws is too small. */
 size_t sig_signature_backward_ex_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, int32_t stream,
                                                 sig_basepoint_t bp, int32_t inverse, int32_t has_initial,

@@ -137,7 +137,7 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
         int64_t maxc = M / kMinChunk;
         pl.n_chunks = want < maxc ? want : maxc;
     }
-    if (pl.n_chunks == 1 && B * cp0 < kOneWave && ks->fwd1) {
+    if (pl.n_chunks == 1 && B * cp0 < kOneWave && ks->fwd1 && !(ks->fwd2 && !stream && B >= kFwd2MinBatch)) {
         pl.P = ks->pf1;
         pl.launch = ks->fwd1;
     }
@@ -397,29 +397,23 @@ struct BwdChunking {
     int64_t m = 1, chunk_len = 0;
 };
 
-// Time chunks of the reversible backward.  Required when one path's increments exceed what a CTA
-// stages in shared memory; optional -- only when the caller gave workspace -- when the batch
-// alone cannot fill the SMs (fewer paths than 148: about 8 CTAs per SM, chunks >= 64 steps).
-// Stream mode is never chunked (every output row feeds the gradient of all earlier steps).
-bool bwd_chunking(const FwdPlan& pl, int64_t B, int32_t stream, bool may_chunk, BwdChunking& ch) {
-    const int64_t maxc = pl.ks->bwd_max_chunk ? pl.ks->bwd_max_chunk() : pl.M;
-    int64_t m = (pl.M + maxc - 1) / maxc;
-    if (stream) {
-        ch.m = 1;
-        ch.chunk_len = pl.M;
-        return m <= 1;
-    }
-    if (m > 1 && !may_chunk) return false;
-    if (may_chunk && B > 0 && B < 148) {
-        // ~8 CTAs per SM: small chunks also stage fewer increments, so more of them co-reside
-        int64_t mo = (8 * 148 + B - 1) / B;
-        const int64_t cap = pl.M / 64 > 1 ? pl.M / 64 : 1;
-        if (mo > cap) mo = cap;
-        if (mo > m) m = mo;
-    }
+// Time chunks of the reversible backward.  K2 stages increments per tile, so any
+// path fits one CTA; chunks only add parallelism.  They are used -- when the caller gave the
+// workspace -- if the batch alone cannot fill one resident wave of the backward (bwd_slots() CTAs
+// per SM, register-limited): then ~one wave of CTAs in total, chunks of >= 64 steps.  Stream mode
+// is never chunked (every output row feeds the gradient of all earlier steps).
+void bwd_chunking(const FwdPlan& pl, int64_t B, int32_t stream, bool may_chunk, BwdChunking& ch) {
+    ch.m = 1;
+    ch.chunk_len = pl.M;
+    if (stream || !may_chunk || B <= 0) return;
+    const int64_t slots = pl.ks->bwd_slots ? pl.ks->bwd_slots() : 0;
+    const int64_t wave = 148 * (slots > 0 ? slots : 8);
+    if (B >= wave || B >= 148 * 4) return;
+    int64_t m = (wave + B - 1) / B;
+    const int64_t cap = pl.M / 64 > 1 ? pl.M / 64 : 1;
+    if (m > cap) m = cap;
     ch.chunk_len = (pl.M + m - 1) / m;
     ch.m = (pl.M + ch.chunk_len - 1) / ch.chunk_len;
-    return true;
 }
 
 size_t bwd_chunk_ws_bytes(const BwdChunking& ch, int64_t B, int64_t S, int64_t C) {
@@ -428,10 +422,47 @@ size_t bwd_chunk_ws_bytes(const BwdChunking& ch, int64_t B, int64_t S, int64_t C
     return align256(5 * rows * (size_t)S * sizeof(float)) + align256(rows * (size_t)C * sizeof(float));
 }
 
-// inclusive ordered product along the chunk axis (Hillis-Steele, ceil(log2 m) launches); the last
-// step writes `out`, the others alternate with tmp
-cudaError_t chunk_scan(const TensorDims& d, const float* in, float* out, float* tmp, int64_t B, int64_t m, int suffix,
-                       cudaStream_t s) {
+// group size of the blocked chunk scan: the largest power of two <= 16 whose group, outputs and
+// carry fit 200 KB of shared memory; 0 when fewer than 4 fit (large S: Hillis-Steele steps in
+// global memory instead)
+int block_scan_group(int64_t S) {
+    int g = 16;
+    while (g >= 4 && (size_t)(2 * g + 1) * S * sizeof(float) > 200 * 1024) g >>= 1;
+    return g >= 4 ? g : 0;
+}
+
+// inclusive ordered product along the chunk axis of in[b*m + j] into out (suffix = 1: from the
+// end).  Blocked (scan_group_t_kernel, compiled per shape): group totals, the scan of the totals
+// (recursively), then every group's inclusive products started from its carry.  For signatures too
+// large for it: Hillis-Steele steps (ceil(log2 m) launches, the last one writing `out`, the others
+// alternating with tmp).  tmp holds rows * S floats (the blocked scan needs < 2/3 of that).
+cudaError_t chunk_scan(const TensorDims& d, ScanLaunch sc, const float* in, float* out, float* tmp, int64_t B, int64_t m,
+                       int suffix, cudaStream_t s) {
+    const int g = block_scan_group(d.S);
+    if (sc != nullptr && g > 0 && m > 1) {
+        const int64_t ng = (m + g - 1) / g;
+        ScanParams p{};
+        p.in = in;
+        p.B = B;
+        p.m = m;
+        p.g = g;
+        p.suffix = suffix;
+        if (ng > 1) {
+            float* T = tmp;                        // [B, ng] group totals
+            float* Ts = T + (size_t)B * ng * d.S;  // [B, ng] their inclusive scan
+            p.tot = T;
+            cudaError_t e = sc(p, s);
+            count_launch();
+            if (e == cudaSuccess) e = chunk_scan(d, sc, T, Ts, Ts + (size_t)B * ng * d.S, B, ng, suffix, s);
+            if (e != cudaSuccess) return e;
+            p.tot = nullptr;
+            p.carry = Ts;
+        }
+        p.out = out;
+        cudaError_t e = sc(p, s);
+        count_launch();
+        return e;
+    }
     int steps = 0;
     for (int64_t o = 1; o < m; o <<= 1) ++steps;
     if (steps == 0) return cudaMemcpyAsync(out, in, (size_t)B * m * d.S * sizeof(float), cudaMemcpyDeviceToDevice, s);
@@ -482,8 +513,8 @@ sig_status_t run_bwd_chunked(const FwdPlan& pl, const BwdChunking& ch, BwdParams
     cudaError_t e = pl.ks->fwd0(f, s);
     if (e != cudaSuccess) return cuda_status(e, "chunk signature launch");
     count_launch();
-    e = chunk_scan(d, units, pin, tmp, B, m, 0, s);
-    if (e == cudaSuccess) e = chunk_scan(d, units, sfx, tmp, B, m, 1, s);
+    e = chunk_scan(d, pl.ks->scan, units, pin, tmp, B, m, 0, s);
+    if (e == cudaSuccess) e = chunk_scan(d, pl.ks->scan, units, sfx, tmp, B, m, 1, s);
     if (e != cudaSuccess) return cuda_status(e, "chunk scan launch");
     const int64_t n = (int64_t)rows * S;
     chunk_gend_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, prm.grad_out, sfx, B, m, gend);
@@ -686,7 +717,7 @@ size_t sig_signature_backward_ex_workspace_size(int64_t B, int64_t L, int64_t C,
                        sizeof(float));
     }
     BwdChunking ch;
-    if (!bwd_chunking(pl, B, stream, true, ch)) return inv;
+    bwd_chunking(pl, B, stream, true, ch);
     return inv + bwd_chunk_ws_bytes(ch, B, (int64_t)S, C);
 }
 
@@ -716,13 +747,7 @@ sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path,
     const size_t full = sig_signature_backward_ex_workspace_size(B, L, C, depth, stream, bp, inverse,
                                                                  initial != nullptr, grad_initial != nullptr);
     const bool roomy = ws != nullptr && ws_bytes >= full;
-    if (!bwd_chunking(pl, B, stream, roomy, ch)) {
-        if (stream)
-            return fail(SIG_ERR_UNSUPPORTED, "stream backward of %lld increments does not fit one CTA's shared memory",
-                        (long long)pl.M);
-        return fail(SIG_ERR_WORKSPACE, "this path needs the time-chunked backward: workspace of %zu bytes needed, "
-                    "%zu given", full, ws_bytes);
-    }
+    bwd_chunking(pl, B, stream, roomy, ch);
     const size_t need = inv_bytes + bwd_chunk_ws_bytes(ch, B, S, C);
     if (ws_bytes < need || (need > 0 && !ws))
         return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need, ws_bytes);

@@ -272,6 +272,17 @@ struct GroupParams {
     int64_t B;               // paths (grid-strided over gridDim.y, which is capped at 65535)
 };
 
+// blocked ordered scan along the chunk axis (scan_group_t_kernel, chunk_block_scan_kernel):
+// elements in[b*m + j] (rows of S floats), groups of g, carries [B, ng]
+struct ScanParams {
+    const float* in;
+    float* out;          // [B, m, S] or nullptr
+    float* tot;          // [B, ng, S] group totals or nullptr
+    const float* carry;  // [B, ng, S] scanned group totals or nullptr
+    int64_t B, m;
+    int g, suffix;
+};
+
 // In-place ordered binary-tree product of cnt signatures gs[0..cnt) (S floats each) held in
 // shared memory by the whole CTA; the result ends in gs[0].  Level by level, top-down: a level-k
 // update of the left operand reads only its levels < k and its own coefficient.

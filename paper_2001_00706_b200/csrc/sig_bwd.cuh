@@ -53,6 +53,7 @@ struct BwdParams {
     int64_t go_stride;       // floats between consecutive units' grad_out rows (non-stream)
     const float* chunk_init; // [B * n_chunks, S]: start state of chunk j >= 1 is row b * n_chunks + j - 1
     float* edge;             // [B * n_chunks, C]: chunk j >= 1 writes its first point's share here
+    int tile;                // sig_bwd_kernel: steps per tile (set by launch_bwd from the occupancy)
 };
 
 // Per-step gz records are flushed every T steps (a CTA barrier each time).  With up to 128 steps
@@ -78,20 +79,27 @@ struct BwdLayout {
     // warp-shuffle reduction applies when C is a power of two dividing 32 and the warps are full
     static constexpr bool FAST = (32 % C == 0) && ((C & (C - 1)) == 0) && (SH::CP % 32 == 0);
     static constexpr int PL = P > 0 ? P : 1;
-    static constexpr int REC = FAST ? C : (C + PL);  // floats per record
+    // floats per record: FAST, one per warp and channel; else one C-vector per thread (the thread
+    // folds its low-level channel partials into their channels before writing)
+    static constexpr int REC = C;
+    // one-warp CTAs (e.g. C=3, N=6 with 27 prefixes) run as time chunks of long paths: ask for 16
+    // resident per SM (<= 128 registers), the latency of one warp's reversal hidden by the others
+    static constexpr int MINB = (NT == 32 && SH::OWN + SH::OWNA <= 64) ? 16 : 1;
     static constexpr int RECS = FAST ? HW : NT;      // records per step
-    __host__ __device__ static int tile(int64_t M) {
-        int T = SIG_BWD_TMAX;
-        while (T > 1 && (size_t)T * RECS * REC * sizeof(float) > SIG_BWD_TILE_KB * 1024) T >>= 1;
-        return (int)(T < M ? T : M);
+    // shared memory of a tile of T steps: the tile's increments, T + 1 record slots, the per-step
+    // totals, gprev, and the low-level partials of grad_initial
+    __host__ __device__ static size_t smem_bytes_tile(int T) {
+        return ((size_t)(T * C + 3) / 4 * 4 + (size_t)(T + 1) * RECS * REC + (size_t)T * C + 32 + (size_t)PL * NT) *
+               sizeof(float);
     }
-    static size_t smem_bytes(int64_t M) {
-        const size_t zf = (size_t)((M * C + 3) / 4 * 4);
-        const size_t T = (size_t)tile(M);
-        return (zf + (T + 1) * RECS * REC + T * C + 32 + (size_t)PL * NT) * sizeof(float);
+    // Largest power-of-two tile (<= SIG_BWD_TMAX, <= M) whose shared memory fits `budget` bytes.
+    // The increments are staged per tile, so the chunk length does not enter: any path fits.
+    static int tile(int64_t M, size_t budget) {
+        int T = SIG_BWD_TMAX;
+        while (T > 1 && smem_bytes_tile(T) > budget) T >>= 1;
+        return (int)(T < M ? T : (M > 0 ? M : 1));
     }
 };
-
 // VJP of the level-K Horner chain, depth-first over the thread's word tree (post-order).
 // Node (I, W) with chain value BI = B_I[p.W] returns beta_I[p.W] = (1/s) sum_c beta_{I+1}[p.W.c] z_c
 // (s = K-I), after adding the level-(I+1) gz contributions (1/s) B_I[p.W] beta_{I+1}[p.W.c] and
@@ -279,7 +287,7 @@ __device__ __forceinline__ void low_tail(float b, const float (&Bp)[SH::PL1], co
 // STREAM (a template flag so that the plain kernel carries no stream-mode register pressure):
 // the gradient w.r.t. every prefix signature, grad_out[t], is added before step t is reversed.
 template <class SH, bool STREAM>
-__global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const BwdParams prm) {
+__global__ void __launch_bounds__(BwdLayout<SH>::NT, BwdLayout<SH>::MINB) sig_bwd_kernel(const BwdParams prm) {
     using LY = BwdLayout<SH>;
     constexpr int C = SH::C, N = SH::N, P = SH::P;
     constexpr int HW = LY::HW;
@@ -290,27 +298,31 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
     const int64_t jc = unit - bidx * prm.n_chunks;       // time chunk
     const int64_t s0 = jc * prm.chunk_len;               // its first increment
     const int64_t M = (prm.chunk_len < prm.M - s0) ? prm.chunk_len : prm.M - s0;  // its increments
-    const int T = LY::tile(M);
-    float* zbuf = sm;                                       // [M][C] increments
-    float* part = zbuf + (prm.chunk_len * C + 3) / 4 * 4;   // [1 + T][RECS][REC] per-step partials
+    const int T = prm.tile;
+    float* zbuf = sm;                                        // [T][C] increments of the current tile
+    float* part = zbuf + (T * C + 3) / 4 * 4;                // [1 + T][RECS][REC] per-step partials
     float* tot = part + (size_t)(T + 1) * LY::RECS * LY::REC;  // [T][C] per-step gz totals
-    float* gprev = tot + (size_t)T * C;                     // [C] gz of the step processed before
-    float* lowred = gprev + 32;                             // [P-1][NT] low-level partials (grad_initial)
+    float* gprev = tot + (size_t)T * C;                      // [C] gz of the step processed before
+    float* lowred = gprev + 32;                              // [P-1][NT] low-level partials (grad_initial)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int has_bp = prm.bp_mode != 0;
     const float* sigrow = prm.sig_final + (size_t)unit * prm.sf_stride;  // state after this unit
 
-    for (int64_t e = tid; e < M * C; e += blockDim.x) {
-        const int64_t s = s0 + e / C;
-        const int c = (int)(e % C);
-        const float* xr = prm.path + bidx * prm.L * C;
-        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
-        const float x1 = xr[r1 * C + c];
-        const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
-        zbuf[e] = prm.zsign * (x1 - x0);
-    }
+    // increments of tile steps j = 0..tn-1 (step t = M-1-(n0+j)) into zbuf[j][c]; the caller
+    // synchronises.  Staged per tile, so shared memory does not grow with the chunk length.
+    const float* xr = prm.path + bidx * prm.L * C;
+    auto stage_tile = [&](int64_t n0, int tn) {
+        for (int e = tid; e < tn * C; e += blockDim.x) {
+            const int j = e / C, c = e % C;
+            const int64_t s = s0 + (M - 1 - (n0 + j));
+            const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
+            const float x1 = __ldg(xr + r1 * C + c);
+            const float x0 = (r0 >= 0) ? __ldg(xr + r0 * C + c) : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
+            zbuf[e] = prm.zsign * (x1 - x0);
+        }
+    };
     if (tid < C) gprev[tid] = 0.0f;
 
     const bool valid = tid < SH::CP;
@@ -375,11 +387,11 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             });
         }
     };
-    auto load_z = [&](int64_t t, float (&z)[C], float (&zp)[SH::PD]) {
+    auto load_z = [&](int j, float (&z)[C], float (&zp)[SH::PD]) {  // tile step j
 #pragma unroll
-        for (int c = 0; c < C; ++c) z[c] = zbuf[t * C + c];
+        for (int c = 0; c < C; ++c) z[c] = zbuf[j * C + c];
 #pragma unroll
-        for (int q = 0; q < SH::PD; ++q) zp[q] = (P > 0) ? zbuf[t * C + p[q]] : 0.0f;
+        for (int q = 0; q < SH::PD; ++q) zp[q] = (P > 0) ? zbuf[j * C + p[q]] : 0.0f;
     };
     // the exact start state at t == 0: the product of the earlier chunks, the user's initial, or 1
     auto start_state = [&]() {
@@ -477,14 +489,21 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
         } else {
             float* r = rec + (size_t)tid * LY::REC;
 #pragma unroll
-            for (int c = 0; c < C; ++c) r[c] = valid ? v[c] : 0.0f;
-#pragma unroll
-            for (int q = 0; q < LY::PL; ++q) r[C + q] = (valid && P > 0) ? acc[q + 1] : 0.0f;
+            for (int c = 0; c < C; ++c) {
+                float vc = v[c];
+                static_for<1, P + 1>([&](auto ic) {  // acc[i] belongs to channel p_{i-1}
+                    constexpr int i = decltype(ic)::value;
+                    if (p[i - 1] == c) vc += acc[i];
+                });
+                r[c] = valid ? vc : 0.0f;
+            }
         }
     };
 
     for (int64_t n0 = 0; n0 < M; n0 += T) {
         const int tn = (int)((M - n0) < T ? (M - n0) : T);
+        stage_tile(n0, tn);
+        __syncthreads();
         // Software pipelining: the gz reduction of step j is issued at the top of step j+1, in the
         // same basic block as that step's arithmetic, so its shuffle latency overlaps the FMAs
         // (the reduction is independent of the next step's state).  The step with t == 0 (exact
@@ -509,7 +528,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
                 reduce_c(reduce_b(v, acc), v, acc, j - 1);
                 stream_add(t);
                 float z[C], zp[SH::PD];
-                load_z(t, z, zp);
+                load_z(j, z, zp);
                 fused_mulexp<SH, N - 1, true>(A, low, z, zp);
                 chains_lower(z, zp, gz, acc);
                 chain_top(z, zp, gz, acc);
@@ -517,7 +536,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             }
             stream_add(t);
             float z[C], zp[SH::PD];
-            load_z(t, z, zp);
+            load_z(j, z, zp);
             float v[C], ac[SH::PL1];  // previous step's gz, reduced while this step computes
 #pragma unroll
             for (int c = 0; c < C; ++c) v[c] = gz[c];
@@ -538,7 +557,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             reduce_c(reduce_b(v, acc), v, acc, tn - 2);
             stream_add(0);
             float z[C], zp[SH::PD];
-            load_z(0, z, zp);
+            load_z(tn - 1, z, zp);
             start_state();
             chains_lower(z, zp, gz, acc);
             chain_top(z, zp, gz, acc);
@@ -559,15 +578,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, 1) sig_bwd_kernel(const Bwd
             if constexpr (LY::FAST) {
                 for (int w = 0; w < HW; ++w) s += rec[w * C + c];
             } else {
-                for (int th = 0; th < SH::CP; ++th) {
-                    const float* r = rec + (size_t)th * LY::REC;
-                    s += r[c];
-                    int q = th;
-                    for (int i = P; i >= 1; --i) {  // r[C + i - 1] belongs to channel p_{i-1}(th)
-                        if (q % C == c) s += r[C + i - 1];
-                        q /= C;
-                    }
-                }
+                for (int th = 0; th < SH::CP; ++th) s += rec[(size_t)th * LY::REC + c];
             }
             tot[j * C + c] = s;
         }
@@ -1245,6 +1256,9 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
 #endif
 
 template <class SH>
+int64_t bwd_slots();
+
+template <class SH>
 cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
     if constexpr (SIG_BWD2 && BwdLayout2<SH>::OK) {
         using LY2 = BwdLayout2<SH>;
@@ -1265,27 +1279,41 @@ cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
         }
     }
     using LY = BwdLayout<SH>;
-    const size_t smem = LY::smem_bytes(prm.chunk_len);
-    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto kern = prm.stream ? sig_bwd_kernel<SH, true> : sig_bwd_kernel<SH, false>;
+    const int slots = bwd_slots<SH>();
+    if (slots <= 0) return cudaErrorInvalidConfiguration;
+    // the shared memory that leaves the register-limited number of CTAs resident (c5's chunked
+    // backward: 1-warp CTAs, 16 per SM), at most SIG_BWD_TILE_KB
+    size_t budget = (size_t)228 * 1024 / slots - 1024;
+    if (budget > (size_t)SIG_BWD_TILE_KB * 1024) budget = (size_t)SIG_BWD_TILE_KB * 1024;
+    BwdParams q = prm;
+    q.tile = LY::tile(prm.chunk_len, budget);
+    const size_t smem = LY::smem_bytes_tile(q.tile);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    kern<<<(unsigned)(prm.B * prm.n_chunks), LY::NT, smem, st>>>(prm);
+    kern<<<(unsigned)(prm.B * prm.n_chunks), LY::NT, smem, st>>>(q);
     return cudaGetLastError();
 }
 
-// Longest chunk (in increments) whose staged increments fit one CTA's shared memory.
+// CTAs of sig_bwd_kernel resident per SM as limited by registers and warps (the tile is then sized
+// so that shared memory does not lower it); 0 if the kernel cannot be queried.
 template <class SH>
-int64_t bwd_max_chunk() {
-    int64_t lo = 1, hi = 1 << 20;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) / 2;
-        if (BwdLayout<SH>::smem_bytes(mid) <= 227 * 1024) lo = mid;
-        else hi = mid - 1;
+int64_t bwd_slots() {
+    static int cached = -1;
+    if (cached < 0) {
+        cudaFuncAttributes a{};
+        if (cudaFuncGetAttributes(&a, sig_bwd_kernel<SH, false>) != cudaSuccess) return 0;
+        constexpr int NT = BwdLayout<SH>::NT;
+        const int regs_per_warp = (a.numRegs * 32 + 255) / 256 * 256;
+        int n = 65536 / (regs_per_warp * (NT / 32));
+        if (n > 64 / (NT / 32)) n = 64 / (NT / 32);
+        if (n > 32) n = 32;
+        cached = n;
     }
-    return lo;
+    return cached;
 }
 
 }  // namespace sigb200

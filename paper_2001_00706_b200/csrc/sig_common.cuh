@@ -194,6 +194,38 @@ __device__ __forceinline__ void add_run(float (&dst)[SZ], const float* src) {
     for (int i = 0; i < n; ++i) dst[OFF + i] += __ldg(src + i);
 }
 
+// Copy n floats global -> shared by the whole CTA with several loads in flight per thread (a plain
+// load-then-store loop serialises one global latency per element: the fold/scan kernels spent most
+// of their time there).  float4 when both sides are 16-byte aligned.
+__device__ __forceinline__ void stage_to_smem(float* __restrict__ dst, const float* __restrict__ src, int n) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const int n4 = n >> 2;
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        int e = tid;
+        for (; e + 3 * nt < n4; e += 4 * nt) {
+            const float4 a = __ldg(s4 + e), b = __ldg(s4 + e + nt), c = __ldg(s4 + e + 2 * nt), d = __ldg(s4 + e + 3 * nt);
+            d4[e] = a;
+            d4[e + nt] = b;
+            d4[e + 2 * nt] = c;
+            d4[e + 3 * nt] = d;
+        }
+        for (; e < n4; e += nt) d4[e] = __ldg(s4 + e);
+        for (int f = (n4 << 2) + tid; f < n; f += nt) dst[f] = __ldg(src + f);
+        return;
+    }
+    int e = tid;
+    for (; e + 3 * nt < n; e += 4 * nt) {
+        const float a = __ldg(src + e), b = __ldg(src + e + nt), c = __ldg(src + e + 2 * nt), d = __ldg(src + e + 3 * nt);
+        dst[e] = a;
+        dst[e + nt] = b;
+        dst[e + 2 * nt] = c;
+        dst[e + 3 * nt] = d;
+    }
+    for (; e < n; e += nt) dst[e] = __ldg(src + e);
+}
+
 // reciprocals 1/s, s = 1..16 (exact float roundings of the rationals)
 __device__ __forceinline__ constexpr float inv_int(int s) {
     return s == 1 ? 1.0f : 1.0f / (float)s;
@@ -224,12 +256,14 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned 
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-// bulk copy of any multiple of 16 bytes, in pieces of at most 64 KB
-__device__ __forceinline__ void bulk_g2s_big(void* sdst, const void* gsrc, size_t bytes, uint64_t* bar) {
+// bulk copy of any multiple of 16 bytes, in pieces of at most `piece` bytes (4 KB vs 64 KB pieces
+// measured the same for c5's 68 KB per CTA)
+__device__ __forceinline__ void bulk_g2s_big(void* sdst, const void* gsrc, size_t bytes, uint64_t* bar,
+                                             unsigned piece = 65536) {
     char* d = static_cast<char*>(sdst);
     const char* g = static_cast<const char*>(gsrc);
     while (bytes > 0) {
-        const unsigned n = bytes > 65536 ? 65536u : (unsigned)bytes;
+        const unsigned n = bytes > piece ? piece : (unsigned)bytes;
         bulk_g2s(d, g, n, bar);
         d += n;
         g += n;

@@ -217,7 +217,65 @@ __device__ __forceinline__ void load_state(const float* row, int prefix, float (
     });
 }
 
-// (a [x] b) at flat coefficient f with compile-time shapes (cf. mul_coef in combine.cuh): the level
+// In-register right product A <- A [x] B for the thread's share of a state (prefix p of length P:
+// own levels >= max(P,1), replicated prefix values low[i] = A_i[p[:i]], i < P), B a full row in
+// shared memory.  (A [x] B)_k[w] = A_k[w] + B_k[w] + sum_{i=1}^{k-1} A_i[w[:i]] B_{k-i}[w[i:]]
+// (eq-tensorproduct): every A factor along the thread's own words is in its registers,
+// every B factor an LDS at a compile-time offset (plus a per-thread base below P).  Levels are
+// updated top-down in place (level k reads only levels < k of A and its own coefficient).
+template <class SH>
+__device__ __forceinline__ void mul_right_regs(float (&own)[SH::OWN], float (&low)[SH::LOWA], const float* Bs,
+                                               int prefix) {
+    constexpr int C = SH::C, N = SH::N, P = SH::P;
+    static_for<0, N - SH::K0 + 1>([&](auto kkc) {
+        constexpr int k = N - decltype(kkc)::value;  // N .. K0
+        constexpr int NW = SH::own(k);                // C^(k-P) owned words p.w'
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            float acc = own[SH::own_off(k) + w] + Bs[SH::lvl_off(k) + prefix * NW + w];
+            static_for<1, k>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                constexpr int D = (int)ipow(C, k - i);  // size of the B block
+                if constexpr (i >= SH::K0) {
+                    acc = fmaf(own[SH::own_off(i) + w / D], Bs[SH::lvl_off(k - i) + w % D], acc);
+                } else {
+                    // A_i[p[:i]] = low[i]; B index (p[i:] . w') = (p mod C^(P-i)) C^(k-P) + w'
+                    const int pb = prefix % (int)ipow(C, P - i);
+                    acc = fmaf(low[i], Bs[SH::lvl_off(k - i) + pb * NW + w], acc);
+                }
+            });
+            own[SH::own_off(k) + w] = acc;
+        }
+    });
+    static_for<0, (P > 1 ? P - 1 : 0)>([&](auto iic) {
+        constexpr int i = P - 1 - decltype(iic)::value;  // P-1 .. 1
+        const int pi = prefix / (int)ipow(C, P - i);      // p[:i]
+        float acc = low[i] + Bs[SH::lvl_off(i) + pi];
+        static_for<1, i>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            const int pj = pi % (int)ipow(C, i - j);      // p[j:i]
+            acc = fmaf(low[j], Bs[SH::lvl_off(i - j) + pj], acc);
+        });
+        low[i] = acc;
+    });
+}
+
+// Ordered fold of the nu consecutive units of a CTA (time order = unit order) with the states in
+// registers: tree level s, unit u = 2sq + s writes its state to shared-memory slot q, unit 2sq
+// multiplies it in from the right (mul_right_regs).  Unit 0 ends with the product.  `slots` holds
+// ceil(nu/2) rows of S floats.  Every thread of the CTA must call it.
+template <class SH>
+__device__ __forceinline__ void fold_units_regs(float (&own)[SH::OWN], float (&low)[SH::LOWA], float* slots, int ul,
+                                                int nu, int prefix) {
+    for (int st = 1; st < nu; st <<= 1) {
+        __syncthreads();  // the previous level's reads of the slots are done
+        if (ul % (2 * st) == st) store_state<SH, false>(slots + (size_t)(ul / (2 * st)) * SH::S, prefix, own, low);
+        __syncthreads();
+        if (ul % (2 * st) == 0 && ul + st < nu) mul_right_regs<SH>(own, low, slots + (size_t)(ul / (2 * st)) * SH::S, prefix);
+    }
+}
+
+// (a [x] b) at flat coefficient f with compile-time shapes// (a [x] b) at flat coefficient f with compile-time shapes (cf. mul_coef in combine.cuh): the level
 // of f selects an unrolled sum whose word splits are divisions by compile-time powers of C.
 template <class SH>
 __device__ __forceinline__ float mul_coef_t(const float* a, const float* b, int f) {
@@ -274,10 +332,10 @@ __global__ void __launch_bounds__(512) fold_group_t_kernel(const GroupParams p) 
     const int64_t j0 = g * p.G;
     const int cnt = (int)((p.n - j0) < p.G ? (p.n - j0) : p.G);
     for (int64_t b = blockIdx.y; b < p.B; b += gridDim.y) {  // gridDim.y is capped at 65535
-        for (int jj = 0; jj < cnt; ++jj) {
-            const float* src = p.in + (j0 + jj) * p.in_sj + b * p.in_sb;
-            float* dst = gs + (size_t)jj * S;
-            for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = __ldg(src + f);
+        if (p.in_sj == S) {
+            stage_to_smem(gs, p.in + j0 * p.in_sj + b * p.in_sb, cnt * S);
+        } else {
+            for (int jj = 0; jj < cnt; ++jj) stage_to_smem(gs + (size_t)jj * S, p.in + (j0 + jj) * p.in_sj + b * p.in_sb, S);
         }
         __syncthreads();
         const float* prod = block_fold_t<SH>(gs, gs + (size_t)p.G * S, cnt);
@@ -285,6 +343,76 @@ __global__ void __launch_bounds__(512) fold_group_t_kernel(const GroupParams p) 
         for (int f = threadIdx.x; f < S; f += blockDim.x) o[f] = prod[f];
         __syncthreads();
     }
+}
+
+// Blocked ordered scan compiled per shape (the time-parallel backward's prefix and suffix products,
+// SURVEY 8(f)1): CTA (grp, b) scans elements grp*g .. grp*g+g-1 of path b sequentially in shared
+// memory, one barrier per element, started from the carry E (the product of all earlier groups for
+// a prefix scan, of all later groups for a suffix scan; none for the first / last group):
+//   prefix: Y_0 = E [x] X_0, Y_i = Y_{i-1} [x] X_i;   suffix: Y_{n-1} = X_{n-1} [x] E, Y_i = X_i [x] Y_{i+1}.
+// Writes Y to out (if given) and the group total (prefix: Y_{n-1}, suffix: Y_0) to tot[b, grp].
+template <class SH>
+__global__ void __launch_bounds__(512) scan_group_t_kernel(const ScanParams p) {
+    extern __shared__ __align__(16) float ss[];  // X[g][S], Y[g][S], E[S]
+    constexpr int S = (int)SH::S;
+    const int g = p.g;
+    const int64_t ng = (p.m + g - 1) / g;
+    const int64_t grp = blockIdx.x;
+    const int64_t j0 = grp * g;
+    const int cnt = (int)((p.m - j0) < g ? (p.m - j0) : g);
+    float* X = ss;
+    float* Y = X + (size_t)g * S;
+    float* E = Y + (size_t)g * S;
+    const bool has_e = p.carry != nullptr && (p.suffix ? grp + 1 < ng : grp > 0);
+    for (int64_t b = blockIdx.y; b < p.B; b += gridDim.y) {
+        stage_to_smem(X, p.in + ((size_t)b * p.m + j0) * S, cnt * S);
+        if (has_e) stage_to_smem(E, p.carry + ((size_t)b * ng + (p.suffix ? grp + 1 : grp - 1)) * S, S);
+        __syncthreads();
+        for (int ii = 0; ii < cnt; ++ii) {
+            const int i = p.suffix ? cnt - 1 - ii : ii;
+            const float* l;
+            const float* r;
+            if (!p.suffix) {
+                l = (i == 0) ? (has_e ? E : nullptr) : Y + (size_t)(i - 1) * S;
+                r = X + (size_t)i * S;
+            } else {
+                l = X + (size_t)i * S;
+                r = (i == cnt - 1) ? (has_e ? E : nullptr) : Y + (size_t)(i + 1) * S;
+            }
+            float* y = Y + (size_t)i * S;
+            if (l == nullptr) {
+                for (int f = threadIdx.x; f < S; f += blockDim.x) y[f] = r[f];
+            } else if (r == nullptr) {
+                for (int f = threadIdx.x; f < S; f += blockDim.x) y[f] = l[f];
+            } else {
+                for (int f = threadIdx.x; f < S; f += blockDim.x) y[f] = mul_coef_t<SH>(l, r, f);
+            }
+            __syncthreads();
+        }
+        if (p.out) {
+            float* dst = p.out + ((size_t)b * p.m + j0) * S;
+            for (int e = threadIdx.x; e < cnt * S; e += blockDim.x) dst[e] = Y[e];
+        }
+        if (p.tot) {
+            const float* t = Y + (size_t)(p.suffix ? 0 : cnt - 1) * S;
+            float* dst = p.tot + ((size_t)b * ng + grp) * S;
+            for (int f = threadIdx.x; f < S; f += blockDim.x) dst[f] = t[f];
+        }
+        __syncthreads();
+    }
+}
+
+template <class SH>
+cudaError_t launch_scan_group_t(const ScanParams& p, cudaStream_t st) {
+    const size_t smem = (size_t)(2 * p.g + 1) * SH::S * sizeof(float);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(scan_group_t_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t ng = (p.m + p.g - 1) / p.g;
+    scan_group_t_kernel<SH><<<dim3((unsigned)ng, p.B < 65535 ? (unsigned)p.B : 65535u), 512, smem, st>>>(p);
+    return cudaGetLastError();
 }
 
 template <class SH>
@@ -299,6 +427,64 @@ cudaError_t launch_fold_group_t(const GroupParams& p, unsigned ngroups, unsigned
     return cudaGetLastError();
 }
 
+// Staging of grouped time chunks held in one tile (see sig_fwd_kernel): one bulk copy of the CTA's
+// contiguous points, then the increments of all its units.
+template <int C>
+__device__ __noinline__ void stage_contig_units(const FwdParams& prm, float* zs, uint64_t* bar, unsigned& stage_phase,
+                                                int64_t unit0, int nu, int T, int has_bp) {
+    float* raw = zs + prm.raw_off;
+    const int64_t b0 = unit0 / prm.n_chunks;
+    const int64_t j0 = unit0 - b0 * prm.n_chunks;
+    const int64_t cl = prm.chunk_len;
+    const int64_t s_lo = j0 * cl;                                               // first increment
+    const int64_t s_hi = ((j0 + nu) * cl < prm.M ? (j0 + nu) * cl : prm.M);    // one past the last
+    const int64_t r_lo = s_lo - has_bp;                                         // its x0 point (-1: basepoint)
+    const float* lo = prm.path + (b0 * prm.L + (r_lo < 0 ? 0 : r_lo)) * C;
+    const float* hi = prm.path + (b0 * prm.L + (s_hi - has_bp) + 1) * C;        // past the last x1
+    const uintptr_t a = reinterpret_cast<uintptr_t>(lo) & ~(uintptr_t)15;
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(hi) + 15) & ~(uintptr_t)15;
+    if (s_hi > s_lo) {
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bar, (unsigned)(e - a));
+            bulk_g2s_big(raw, reinterpret_cast<const void*>(a), e - a, bar);
+        }
+        mbar_wait(bar, stage_phase);
+        stage_phase ^= 1u;
+    }
+    const float* base = raw + ((reinterpret_cast<uintptr_t>(lo) & 15) >> 2);  // point max(r_lo, 0)
+    const int TC = T * C;
+    for (int uu = 0; uu < nu; ++uu) {  // per unit: no division in the element loop
+        const int64_t su = (j0 + uu) * cl;  // the unit's first increment
+        const int64_t rem = s_hi - su;
+        const int len = (int)(rem <= 0 ? 0 : (rem < cl ? rem : cl));
+        const int64_t rel0 = su - s_lo + (r_lo < 0 ? -1 : 0);  // its first x0 row relative to base
+        const float* ub = base + rel0 * C;
+        float* zu = zs + (size_t)uu * TC;
+        for (int i = threadIdx.x; i < TC; i += blockDim.x) {
+            float zv = 0.0f;
+            if (i < len * C) {
+                const float x1 = ub[i + C];
+                float x0;
+                if (rel0 >= 0 || i >= C) x0 = ub[i];
+                else x0 = (prm.bp_mode == 2) ? prm.basepoint[b0 * C + i] : 0.0f;  // the path's first x0
+                zv = prm.zsign * (x1 - x0);
+            }
+            const int t = i / C, c = i - t * C;
+            zu[t * C + zswz(C, c)] = zv;
+        }
+    }
+}
+
+// in-CTA fold of grouped time chunks with the states in registers (fold_units_regs); 0: the
+// shared-memory tree fold block_fold_t
+#ifndef SIG_FOLD_REGS
+#define SIG_FOLD_REGS 1
+#endif
+// grouped chunks in one tile: one bulk copy of the CTA's contiguous points (0: one per unit)
+#ifndef SIG_FWD_CONTIG
+#define SIG_FWD_CONTIG 1
+#endif
 template <class SH>
 __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     constexpr int C = SH::C;
@@ -336,7 +522,14 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
     if (prm.raw_off > 0 && threadIdx.x == 0) mbar_init(&stage_bar, 1);
     for (int64_t t0 = 0; t0 < prm.chunk_len; t0 += T) {
         __syncthreads();
-        if (prm.raw_off > 0) {
+        if (SIG_FWD_CONTIG && prm.raw_off > 0 && prm.upc > 0 && T >= prm.chunk_len) {
+            // ---- TMA, grouped chunks in one tile: the CTA's units are consecutive chunks of one
+            // path, so their points are ONE contiguous run -- one bulk copy, then all threads form
+            // the increments of all units at once (a copy and a serial loop per unit cost c1's
+            // latency plan ~0.4 us per unit; c1 10.3 -> 6.2 us per call).  Out of line so that it
+            // does not enter the register allocation of the scan loop.
+            stage_contig_units<C>(prm, zs, &stage_bar, stage_phase, unit0, nu, T, has_bp);
+        } else if (prm.raw_off > 0) {
             // ---- TMA: the 16-byte-aligned cover of every unit's rows, one bulk copy per unit
             float* raw = zs + prm.raw_off;
             const int64_t ru = RawLayout::unit(T, C);
@@ -469,12 +662,17 @@ __global__ void __launch_bounds__(512, 1) sig_fwd_kernel(const FwdParams prm) {
         // grouped time chunks: this CTA's units are consecutive chunks of one path; fold
         // their signatures in time order in shared memory (Chen's identity, eq-grouplike) and write
         // one partial product.  Units past the end hold the identity (zero state).
+#if SIG_FOLD_REGS
+        fold_units_regs<SH>(own, low, zs, ul, nu, prefix);
+        if (ul == 0) store_state<SH, false>(prm.out + (size_t)blockIdx.x * SH::S, prefix, own, low);
+#else
         __syncthreads();
         store_state<SH, false>(zs + (size_t)ul * SH::S, prefix, own, low);
         __syncthreads();
         const float* prod = block_fold_t<SH>(zs, zs + (size_t)nu * SH::S, nu);
         float* o = prm.out + (size_t)blockIdx.x * SH::S;
         for (int f = threadIdx.x; f < (int)SH::S; f += blockDim.x) o[f] = prod[f];
+#endif
         return;
     }
     if (valid && !prm.stream) store_state<SH, false>(prm.out + (size_t)unit * SH::S, prefix, own, low);
@@ -709,11 +907,15 @@ __global__ void __launch_bounds__(FwdLayout2<SH>::NT, 1) sig_fwd2_kernel(const F
 #define SIG_FWD2 1
 #endif
 
+// The two-prefix forward runs one CTA per path: from 64 paths on it beats the wider-prefix
+// variant (c2's shape at B = 128: 0.140 ms with P = 4, one CTA per path of 256 threads ~0.04 ms).
+constexpr int64_t kFwd2MinBatch = 64;
+
 template <class SH>
 cudaError_t launch_fwd(const FwdParams& prm_in, cudaStream_t st) {
     if constexpr (SIG_FWD2 && FwdLayout2<SH>::OK) {
         if (!prm_in.stream && prm_in.n_chunks == 1 && prm_in.upc == 0 && prm_in.initial == nullptr &&
-            prm_in.B >= 148) {
+            prm_in.B >= kFwd2MinBatch) {
             FwdParams prm = prm_in;
             prm.tile = (int)(prm.M < 256 ? prm.M : 256);
             const size_t smem = (size_t)prm.tile * SH::C * sizeof(float);

@@ -8,19 +8,23 @@ namespace sigb200 {
 struct FwdParams;
 struct BwdParams;
 struct GroupParams;
+struct ScanParams;
 
 using FwdLaunch = cudaError_t (*)(const FwdParams&, cudaStream_t);
 using BwdLaunch = cudaError_t (*)(const BwdParams&, cudaStream_t);
-using BwdMaxChunk = int64_t (*)();
+using BwdSlots = int64_t (*)();
 using FoldLaunch = cudaError_t (*)(const GroupParams&, unsigned ngroups, unsigned B, cudaStream_t);
+using ScanLaunch = cudaError_t (*)(const ScanParams&, cudaStream_t);
 
 struct KernelSet {
     int C, N;
     int pf0, pf1, pb;   // prefix lengths of the two forward variants and of the backward (-1: none)
     FwdLaunch fwd0, fwd1;
     BwdLaunch bwd;
-    BwdMaxChunk bwd_max_chunk;  // longest time chunk the backward stages in shared memory
+    BwdSlots bwd_slots;         // CTAs of the (chunk-capable) backward resident per SM
     FoldLaunch fold;            // compiled ordered group fold (K3) for this (C, N)
+    ScanLaunch scan;            // compiled blocked chunk scan (the time-parallel backward)
+    bool fwd2;                  // fwd0 has the two-prefix forward (sig_fwd2_kernel, plain calls of B >= 64)
 };
 
 const KernelSet* kernels_c1(int N);

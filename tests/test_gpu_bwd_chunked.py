@@ -32,8 +32,8 @@ def test_small_batch_chunked_backward(C, N, B, L):
     assert err < BWD_TOL
 
 
-def test_long_path_requires_chunks():
-    """One path longer than a CTA can stage (previously UNSUPPORTED): chunking is mandatory."""
+def test_long_path_chunked():
+    """One long path (40000 points): split into time chunks for parallelism."""
     C, N, B, L = 3, 4, 1, 40000
     x = brownian_paths(B, L, C, seed=9)
     S = sb.sig_signature_channels(C, N)
@@ -72,3 +72,25 @@ def test_chunked_backward_is_deterministic():
     a, _ = sb.sig_signature_backward(g, x, out, N)
     b, _ = sb.sig_signature_backward(g, x, out, N)
     assert torch.equal(a, b)
+
+
+def test_long_path_unchunked_plain_call():
+    """The plain C call sig_signature_backward (no workspace, so no time chunks) on a path far
+    longer than one CTA could stage whole: K2 stages its increments tile by tile (K2)."""
+    C, N, B, L = 3, 4, 2, 40000
+    x = brownian_paths(B, L, C, seed=19)
+    S = sb.sig_signature_channels(C, N)
+    g = normal((B, S), 20)
+    xt = _cuda(x)
+    gt = _cuda(g)
+    out = sb.sig_signature(xt, N)
+    gp = torch.empty_like(xt)
+    Lib = sb.lib()
+    st = Lib.sig_signature_backward(sb._ptr(gt), sb._ptr(xt), sb._ptr(out), B, L, C, N, 0, sb.BP_NONE, None,
+                                    sb._ptr(gp), None, sb._stream(xt.device))
+    assert st == 0, Lib.sig_last_error()
+    torch.cuda.synchronize()
+    ref, _ = oracle.signature_vjp(g, x, N)
+    err = path_rel_err(gp.cpu().numpy(), ref)
+    print(f"PARITY unchunked long-path bwd: {err:.3e}")
+    assert err < BWD_TOL

@@ -296,7 +296,13 @@ def test_c5_full_size_backward_sampled():
     [e_j, e_{j+1}]), their ordered prefix products P_j and suffix products Q_j, and for three sampled
     chunks the gradient at the chunk's end (the left-operand VJP of P_{j+1} [x] Q_j at grad_out) and
     then the chunk's own VJP started from P_j (signature_vjp_ex with initial) -- the exact gradient
-    of the chunk's interior points.  Bar: 5e-4 of the sampled gradient's max norm."""
+    of the chunk's interior points.
+    Bars (R9, R21), 5e-4 each:
+      * increment gradients dL/dz_t of every sampled chunk, per chunk (||.||inf / ||ref||inf): the
+        GPU's are recovered exactly from its point gradients by a float64 prefix sum (dL/dz_t =
+        -sum_{s<=t} dL/dx_s; each dL/dx_s was formed as a float32 difference of two dL/dz);
+      * point gradients dL/dx per path (R9): normalised by the path's ||ref||inf, bounded below by
+        the sampled chunks' values and the two end points' gradients (a stricter normaliser)."""
     from concurrent.futures import ThreadPoolExecutor
 
     C, N, L = 3, 6, 2 ** 22
@@ -304,12 +310,14 @@ def test_c5_full_size_backward_sampled():
     g = normal((1, oracle.sig_channels(C, N)), seed=105)
     xt = _cuda(x)
     gp, _ = sb.sig_signature_backward(_cuda(g), xt, sb.sig_signature(xt, N), N)
-    gp = gp.cpu().numpy()
+    gp = gp.cpu().numpy().astype(np.float64)
+    gz_gpu = -np.cumsum(gp[0], axis=0)[:-1]  # [M, C]
     nch, M = 256, L - 1
     e = [round(j * M / nch) for j in range(nch + 1)]
     with ThreadPoolExecutor(16) as ex:  # the oracle's C calls release the GIL
         sigs = list(ex.map(lambda j: oracle.signature(x[:, e[j]:e[j + 1] + 1], N)[0], range(nch)))
     sigs = np.stack(sigs)
+    refs = {}
     for j in (0, 137, nch - 1):
         P = oracle.multi_combine(sigs[:j, None], C, N)[0] if j > 0 else None
         Pn = oracle.multi_combine(sigs[:j + 1, None], C, N)[0]
@@ -320,7 +328,19 @@ def test_c5_full_size_backward_sampled():
             gend = g[0].astype(np.float64)
         ref, _, _ = oracle.signature_vjp_ex(gend[None], x[:, e[j]:e[j + 1] + 1], N,
                                             initial=None if P is None else P[None])
+        refs[j] = ref[0]
+        gz_ref = -np.cumsum(ref[0], axis=0)[:-1]  # increments e_j .. e_{j+1}-1 (ref[0][0] = -dL/dz_{e_j})
+        ez = float(np.max(np.abs(gz_gpu[e[j]:e[j + 1]] - gz_ref)) / np.max(np.abs(gz_ref)))
+        print(f"PARITY c5 full-size backward, chunk {j}: increment gradient {ez:.3e}")
+        assert ez < BWD_TOL, (j, ez)
+    # the path's gradient norm: at least the sampled chunks' interior values and the end points
+    # (dL/dx_0 = -dL/dz_0 and dL/dx_M = dL/dz_{M-1}, exact in the first / last chunk's VJP)
+    den = max(max(float(np.max(np.abs(r))) for r in refs.values()),
+              float(np.max(np.abs(refs[0][0]))), float(np.max(np.abs(refs[nch - 1][-1]))))
+    for j, r in refs.items():
         a, b = e[j] + 1, e[j + 1]  # interior points only (boundary points get shares of two chunks)
-        err = path_rel_err(gp[:, a:b], ref[:, 1:-1])
-        print(f"PARITY c5 full-size backward, chunk {j}: {err:.3e}")
-        assert err < BWD_TOL, (j, err)
+        ex_ = float(np.max(np.abs(gp[0, a:b] - r[1:-1]))) / den
+        print(f"PARITY c5 full-size backward, chunk {j}: point gradient (per path, R9) {ex_:.3e}")
+        assert ex_ < BWD_TOL, (j, ex_)
+    assert float(np.max(np.abs(gp[0, 0] - refs[0][0]))) / den < BWD_TOL
+    assert float(np.max(np.abs(gp[0, -1] - refs[nch - 1][-1]))) / den < BWD_TOL
