@@ -171,6 +171,8 @@ def _oracle_step(oracle, cfg_name, x, gs, threads):
         from oracle import lyndon
         g = normal((x.shape[0], lyndon.witt(C, N)), gs)
         oracle.logsignature_vjp(g, x, N, mode="words", threads=threads)
+    elif cfg["op"] == "logsig_stream_fwd":
+        oracle.logsignature(x, N, mode="words", stream=True, threads=threads)
     else:
         oracle.signature(x, N, stream=cfg["stream"], threads=threads)
 
@@ -304,6 +306,9 @@ class Workload:
             ws += self.B * self.M * self.S * 4
         elif cfg["op"] == "logsig_words_fwd_bwd":
             ws += self.B * self.S * 4 * 4
+        elif cfg["op"] == "logsig_stream_fwd":
+            self.W = sb.sig_logsignature_channels(self.C, self.N, "words")
+            ws += self.B * self.M * (self.S + self.W) * 4
         self.working_set = ws
         self.flush = ws <= L2_BYTES
         self.graph = name == "c1"  # latency-bound: replay the step from a CUDA graph (time_workload)
@@ -332,6 +337,9 @@ class Workload:
             mark("fwd")
             res, _ = sb.sig_logsignature_backward(g, x, sig, N, "words")
             mark("bwd")
+        elif op == "logsig_stream_fwd":
+            res = sb.sig_logsignature(x, N, "words", stream=True)
+            mark("fwd")
         elif op == "sig_fwd_timechunk":
             from paper_2001_00706_b200 import dist as sdist
 
@@ -412,6 +420,21 @@ class Workload:
                  "step_frac": (f_fwd + f_bwd) / (ms_step / 1000) / 1e12 / peak}
             r.update(meas(ach))
             return r
+        if op == "logsig_stream_fwd":
+            hbm = 6543.7
+            try:
+                hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            except Exception:
+                pass
+            # the step's DRAM bytes as built: K1 stream writes every prefix signature (B M S floats),
+            # K4 reads them back and writes the words (B M w floats); the path read is negligible
+            rows = B * M
+            nbytes = (2 * rows * self.S + rows * self.W) * 4 + B * self.L * C * 4
+            ach = nbytes / (seg_ms["fwd"] / 1000) / 1e9
+            return {"bound": "hbm", "kernel": "sig_fwd_stream_kernel + logsig_fwd_t_kernel (stream logsignature, "
+                    "bytes of both kernels)", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel_ms": seg_ms["fwd"],
+                    "output_gbs": rows * self.W * 4 / (seg_ms["fwd"] / 1000) / 1e9}
         if op == "sig_fwd_stream":
             hbm = 6543.7
             try:
@@ -659,7 +682,7 @@ def run_ours(args, rank: int, world: int):
     # every other BASELINE config, bounded, in the same run (c1 is a single-GPU row)
     if not args.no_configs:
         blk = {}
-        for name in ("c1", "c2", "c3", "c4", "c5", "c5b"):
+        for name in ("c1", "c2", "c3", "c4", "c5", "c5b", "c3l"):
             if name == args.config or (name == "c1" and world > 1):
                 continue
             blk[name] = measure_config(name, rank, world, dev, min(args.steps, 50), args.warmup)

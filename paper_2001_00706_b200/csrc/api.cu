@@ -14,6 +14,7 @@
 #include "combine.cuh"
 #include "logsig.cuh"
 #include "logsig_owned.cuh"
+#include "logsig_rows.cuh"
 #include "lyndon.h"
 #include "sig_bwd.cuh"
 #include "sig_table.h"
@@ -550,6 +551,20 @@ sig_status_t launch_logsig_fwd(const sig_logsig_plan_s* plan, const float* sig, 
     p.rows = rows;
     p.sig = sig;
     p.out = out;
+    if (rows == 0) return ok();
+    // many small rows (stream mode): one warp per row (logsig_rows.cuh) when its slice of shared
+    // memory is small; big rows keep a CTA each
+    LogsigRowsLaunch rl = find_logsig_rows_t(plan->C, plan->N);
+    if (rows >= 8 * 148 &&
+        (rl != nullptr || logsig_rows_warp_floats(p.d, (int)plan->w, p.mode == 1) * sizeof(float) <= 24 * 1024)) {
+        cudaError_t e = rl ? rl(p, s) : launch_logsig_rows(p, s);
+        if (e == cudaSuccess) {
+            count_launch();
+            return ok();
+        }
+        if (e != cudaErrorInvalidConfiguration) return cuda_status(e, "logsig rows launch");
+        (void)cudaGetLastError();
+    }
 #if !defined(SIG_LOGSIG_FWD_GENERIC)
     if (LogsigFwdLaunch fn = find_logsig_fwd_t(plan->C, plan->N)) {
         cudaError_t e = fn(p, s);

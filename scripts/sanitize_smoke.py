@@ -27,5 +27,21 @@ x4 = cu(brownian_paths(3, 20, 4, 8))
 for mode in ("words", "brackets", "expand"):
     o, sg = sb.sig_logsignature(x4, 5, mode, return_signature=True)
     sb.sig_logsignature_backward(cu(normal(tuple(o.shape), 9)), x4, sg, 5, mode)
+# round 2: prefix-pair K2 (c2's shape), latency plan with the register fold (c1's shape), one-warp
+# chunked K2 with per-tile staging and the compiled blocked scans (C=3, N=6), plain unchunked long
+# backward (C API without workspace)
+x5 = cu(brownian_paths(150, 12, 8, 10))
+s5 = sb.sig_signature(x5, 5)
+sb.sig_signature_backward(cu(normal((150, s5.shape[1]), 11)), x5, s5, 5)
+x6 = cu(brownian_paths(4, 128, 4, 12))
+sb.sig_signature(x6, 4)
+x7 = cu(brownian_paths(1, 20000, 3, 13))
+s7 = sb.sig_signature(x7, 6)
+sb.sig_signature_backward(cu(normal((1, s7.shape[1]), 14)), x7, s7, 6)
+g7 = cu(normal((1, s7.shape[1]), 15))
+gp7 = torch.empty_like(x7)
+Lib = sb.lib()
+assert Lib.sig_signature_backward(sb._ptr(g7), sb._ptr(x7), sb._ptr(s7), 1, 20000, 3, 6, 0, sb.BP_NONE, None,
+                                  sb._ptr(gp7), None, sb._stream(x7.device)) == 0
 torch.cuda.synchronize()
 print("ok")

@@ -16,7 +16,8 @@ from __future__ import annotations
 import numpy as np
 
 # Per-config seeds: path seed / grad seed.
-SEEDS = {"c1": (1, None), "c2": (2, 102), "c3": (3, None), "c4": (4, 104), "c5": (5, None), "c5b": (5, 105)}
+SEEDS = {"c1": (1, None), "c2": (2, 102), "c3": (3, None), "c4": (4, 104), "c5": (5, None), "c5b": (5, 105),
+         "c3l": (3, None)}
 
 # BASELINE.json configs
 CONFIGS = {
@@ -27,6 +28,8 @@ CONFIGS = {
     "c5": dict(B=1, L=2 ** 22, C=3, N=6, stream=False, op="sig_fwd_timechunk"),
     # not a BASELINE config: c5's path through forward + reversible backward
     "c5b": dict(B=1, L=2 ** 22, C=3, N=6, stream=False, op="sig_fwd_bwd_timechunk"),
+    # not a BASELINE config: stream-mode logsignature (words) at c3's shape
+    "c3l": dict(B=256, L=1024, C=6, N=4, stream=True, op="logsig_stream_fwd"),
 }
 
 

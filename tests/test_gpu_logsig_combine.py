@@ -203,3 +203,33 @@ def test_multi_combine_fold_paths(C, N, n):
     got = sb.multi_signature_combine(_cuda(sigs), C, N).cpu().numpy()
     ref = oracle.multi_combine(sigs, C, N)
     assert level_rel_err(got, ref, C, N) < FWD_TOL
+
+
+@pytest.mark.parametrize("mode", ["words", "brackets", "expand"])
+@pytest.mark.parametrize("C,N,B,L", [(6, 4, 3, 600), (3, 5, 2, 700), (4, 4, 2, 800), (8, 3, 4, 400)])
+def test_logsignature_stream_many_rows(mode, C, N, B, L):
+    """Stream-mode logsignature with more than 8 x 148 rows: K4 runs one warp per row
+    (logsig_rows.cuh).  Against the oracle's log of its own signature rounded to float32 (R20)."""
+    x = brownian_paths(B, L, C, seed=60 + C)
+    w = sb.sig_logsignature_channels(C, N, mode)
+    assert B * (L - 1) >= 8 * 148
+    got = sb.logsignature(_cuda(x), N, mode, stream=True).cpu().numpy().reshape(-1, w)
+    sig32 = oracle.signature(x, N, stream=True).astype(np.float32).reshape(-1, sb.sig_signature_channels(C, N))
+    rows = np.r_[0:64, sig32.shape[0] - 64:sig32.shape[0], 500:sig32.shape[0]:97]  # sampled rows, both ends
+    ref32 = oracle.logsignature_from_signature(sig32[rows], C, N, mode)
+    err = block_rel_err(got[rows], ref32, _blocks(C, N, mode))
+    print(f"PARITY stream logsig many rows C={C} N={N} {mode}: {err:.3e}")
+    assert err < FWD_TOL
+
+
+def test_logsignature_rows_kernel_matches_per_row_kernel():
+    """The warp-per-row K4 and the CTA-per-row K4 compute the same log of the same rows (the row
+    count alone selects the kernel): bitwise equality is not required (summation order is the
+    same, float64), but agreement to float32 rounding."""
+    C, N = 6, 4
+    S = sb.sig_signature_channels(C, N)
+    sig = oracle.signature(brownian_paths(4, 400, C, seed=70), N, stream=True).astype(np.float32).reshape(-1, S)
+    many = sb.sig_logsignature_from_signature(_cuda(sig), C, N, "words").cpu().numpy()
+    few = np.concatenate([sb.sig_logsignature_from_signature(_cuda(sig[i:i + 100]), C, N, "words").cpu().numpy()
+                          for i in range(0, sig.shape[0], 100)])
+    np.testing.assert_allclose(many, few, rtol=2e-6, atol=1e-7)
