@@ -649,7 +649,7 @@ def measure_config(name, rank, world, dev, steps, warmup, scaling="weak", batch=
 def run_ours(args, rank: int, world: int):
     import torch
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", _local_gpu())
     all_cpus = os.sched_getaffinity(0)
     bind_gpu_local_cpus(dev.index)
     torch.cuda.set_device(dev)
@@ -718,6 +718,15 @@ def run_dry(args, rank: int, world: int):
                           "backend": args.backend, "scaling": args.scaling}), flush=True)
 
 
+def _local_gpu() -> int:
+    """This rank's GPU: LOCAL_RANK.  Dev check only: SIGB200_BENCH_SHARE_GPU=1 puts every rank on
+    cuda:0 (with --backend gloo) to exercise the N-rank path of this script on a one-GPU box; the
+    numbers of such a run are not a measurement of N GPUs."""
+    if os.environ.get("SIGB200_BENCH_SHARE_GPU") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", 0))
+
+
 def _free_port() -> int:
     import socket
 
@@ -768,7 +777,7 @@ def main():
         import torch.distributed as dist
 
         if not args.dry_run:
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            torch.cuda.set_device(_local_gpu())
         dist.init_process_group(args.backend)
     try:
         (run_dry if args.dry_run else run_ours)(args, rank, world)

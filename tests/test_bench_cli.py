@@ -38,3 +38,20 @@ def test_bench_refuses_mismatched_world():
     r = _run(["--gpus", "4", "--dry-run", "--steps", "3"], env={"WORLD_SIZE": "2", "RANK": "0"})
     assert r.returncode != 0
     assert "WORLD_SIZE" in (r.stderr + r.stdout)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,scaling", [("c2", "strong"), ("c5", "weak")])
+def test_bench_world2_real_kernels_one_gpu(config, scaling):
+    """The N-rank path of bench.py with the real kernels: two ranks share cuda:0 over gloo
+    (SIGB200_BENCH_SHARE_GPU=1; the multi-GPU NCCL box is not available to this build).  Checks
+    that the arm runs end to end (batch shards, or c5's time chunks with the all-gather and ordered
+    fold) and rank 0 prints one line with n_gpus = 2 -- not a measurement of two GPUs."""
+    r = _run(["--gpus", "2", "--backend", "gloo", "--config", config, "--scaling", scaling, "--steps", "3",
+              "--warmup", "3", "--no-configs", "--no-cpu-baseline"], env={"SIGB200_BENCH_SHARE_GPU": "1"}, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1, r.stdout
+    ln = lines[0]
+    assert ln["n_gpus"] == 2 and ln["value"] > 0 and ln["gpu_launches"] > 0
+    assert ln["scaling"] == ("strong" if config == "c5" else scaling)
