@@ -54,7 +54,44 @@ struct BwdParams {
     const float* chunk_init; // [B * n_chunks, S]: start state of chunk j >= 1 is row b * n_chunks + j - 1
     float* edge;             // [B * n_chunks, C]: chunk j >= 1 writes its first point's share here
     int tile;                // sig_bwd_kernel: steps per tile (set by launch_bwd from the occupancy)
+    int64_t raw_off;         // > 0 (two-prefix kernels): the path's points are bulk-copied by TMA into
+                             // shared memory at this float offset and the increments formed there
 };
+
+// Increments of one whole path into zbuf[M][C] (the two-prefix K2 kernels).  raw_off > 0: the
+// 16-byte-aligned cover of the path's L points arrives by TMA bulk copies (cp.async.bulk, one
+// mbarrier) and the increments are formed from shared memory; else coalesced loads from global.
+// The caller synchronises the CTA afterwards.
+template <int C>
+__device__ __forceinline__ void stage_path_increments(const BwdParams& prm, int64_t bidx, int64_t M, float* zbuf,
+                                                      float* smem_base, uint64_t* bar) {
+    const int tid = threadIdx.x;
+    const int has_bp = prm.bp_mode != 0;
+    const float* xr = prm.path + bidx * prm.L * C;
+    const float* base = xr;
+    if (prm.raw_off > 0) {
+        float* raw = smem_base + prm.raw_off;
+        const uintptr_t a = reinterpret_cast<uintptr_t>(xr) & ~(uintptr_t)15;
+        const uintptr_t e = (reinterpret_cast<uintptr_t>(xr + prm.L * C) + 15) & ~(uintptr_t)15;
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bar, (unsigned)(e - a));
+            bulk_g2s_big(raw, reinterpret_cast<const void*>(a), e - a, bar);
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        mbar_wait(bar, 0);
+        base = raw + ((reinterpret_cast<uintptr_t>(xr) & 15) >> 2);
+    }
+    for (int64_t e = tid; e < M * C; e += blockDim.x) {
+        const int64_t s = e / C;
+        const int c = (int)(e % C);
+        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
+        const float x1 = base[r1 * C + c];
+        const float x0 = (r0 >= 0) ? base[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
+        zbuf[e] = prm.zsign * (x1 - x0);
+    }
+}
 
 // Per-step gz records are flushed every T steps (a CTA barrier each time).  With up to 128 steps
 // per tile a c2/c4 path has a single flush, so the warps run the whole reversal without a barrier.
@@ -681,6 +718,8 @@ struct BwdLayout2 {
         const size_t T = (size_t)tile(M);
         return (zf + T * HW * C + T * C + 32) * sizeof(float);
     }
+    // floats of the TMA staging area for a path of L points (its 16-byte-aligned cover)
+    static size_t raw_floats(int64_t L) { return (size_t)((L * C + 8 + 3) / 4 * 4); }
 };
 
 // the prefix chain of chain K up to level J (J <= P-1): Bp[j] = B^(K)_j[p[:j]], j = 1..J (Bp[0] = 1)
@@ -714,15 +753,8 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2_kernel(const B
     const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;
     const float* gorow = prm.grad_out + (size_t)bidx * prm.go_stride;
 
-    for (int64_t e = tid; e < M * C; e += blockDim.x) {
-        const int64_t s = e / C;
-        const int c = (int)(e % C);
-        const float* xr = prm.path + bidx * prm.L * C;
-        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
-        const float x1 = xr[r1 * C + c];
-        const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
-        zbuf[e] = prm.zsign * (x1 - x0);
-    }
+    __shared__ uint64_t stage_bar;
+    stage_path_increments<C>(prm, bidx, M, zbuf, sm, &stage_bar);
     if (tid < C) gprev[tid] = 0.0f;
 
     const int pa = 2 * tid;  // prefixes pa, pa + 1 (siblings: same p[:P-1], last digit p[P-1], p[P-1] + 1)
@@ -962,16 +994,9 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
     const int has_bp = prm.bp_mode != 0;
     const float* sigrow = prm.sig_final + (size_t)bidx * prm.sf_stride;
     const float* gorow = prm.grad_out + (size_t)bidx * prm.go_stride;
-    const float* xr = prm.path + bidx * prm.L * C;
 
-    for (int64_t e = tid; e < M * C; e += blockDim.x) {
-        const int64_t s = e / C;
-        const int c = (int)(e % C);
-        const int64_t r1 = s + 1 - has_bp, r0 = s - has_bp;
-        const float x1 = xr[r1 * C + c];
-        const float x0 = (r0 >= 0) ? xr[r0 * C + c] : ((prm.bp_mode == 2) ? prm.basepoint[bidx * C + c] : 0.0f);
-        zbuf[e] = prm.zsign * (x1 - x0);
-    }
+    __shared__ uint64_t stage_bar;
+    stage_path_increments<C>(prm, bidx, M, zbuf, sm, &stage_bar);
     if (tid < C) gprev[tid] = 0.0f;
 
     const int pa = 2 * tid;  // prefixes pa, pa + 1: same p[:P-1], last digits p[P-1], p[P-1] + 1
@@ -1251,6 +1276,9 @@ __global__ void __launch_bounds__(BwdLayout2<SH>::NT, 1) sig_bwd2p_kernel(const 
 #ifndef SIG_BWD2
 #define SIG_BWD2 1
 #endif
+#ifndef SIG_BWD_TMA_STAGE
+#define SIG_BWD_TMA_STAGE 1
+#endif
 #ifndef SIG_BWD2P
 #define SIG_BWD2P 1
 #endif
@@ -1269,11 +1297,22 @@ cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
                 size_t smem = smem2;
                 unsigned grid = (unsigned)prm.B;
                 if constexpr (SIG_BWD2P && BwdLayout2P<SH>::OK) kern = sig_bwd2p_kernel<SH>;
+                BwdParams q = prm;
+                q.raw_off = 0;
+                // TMA staging of the points when the cover stays inside the path tensor (16-byte
+                // aligned start and end) and fits next to the rest
+                const bool aligned = (reinterpret_cast<uintptr_t>(prm.path) & 15) == 0 && (prm.B * prm.L * SH::C) % 4 == 0;
+                const int64_t roff = ((int64_t)(smem2 / sizeof(float)) + 3) / 4 * 4;  // 16-byte aligned
+                const size_t with_raw = ((size_t)roff + LY2::raw_floats(prm.L)) * sizeof(float);
+                if (SIG_BWD_TMA_STAGE && aligned && with_raw <= 227 * 1024) {
+                    q.raw_off = roff;
+                    smem = with_raw;
+                }
                 if (smem > 48 * 1024) {
                     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     if (e != cudaSuccess) return e;
                 }
-                kern<<<grid, LY2::NT, smem, st>>>(prm);
+                kern<<<grid, LY2::NT, smem, st>>>(q);
                 return cudaGetLastError();
             }
         }
