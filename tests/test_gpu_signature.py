@@ -121,6 +121,9 @@ BWD_CASES = [
     (4, 4, 160, 700, False),
     (8, 5, 150, 200, False),
     (6, 4, 2, 300, True),
+    # B just above one resident wave of one-CTA-per-SM kernels (a partial last wave)
+    (4, 7, 150, 130, False),
+    (8, 5, 158, 140, False),
 ]
 
 
