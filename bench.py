@@ -413,7 +413,7 @@ class Workload:
                     "sig_fwd_bwd_timechunk": "time-parallel reversible backward (chunk signatures, ordered scans, "
                                              "chunk-end VJPs, sig_bwd_kernel over all chunks)"}[op]
             r = {"bound": "alu", "kernel": kern, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                 "frac": ach / peak, "traffic": traffic.get("sig_bwd_kernel"), "peak_source": peak_src,
+                 "frac": ach / peak, "traffic": traffic.get("dominant_kernel"), "peak_source": peak_src,
                  "kernel_ms": seg_ms["bwd"], "step_share": seg_ms["bwd"] / (seg_ms["fwd"] + seg_ms["bwd"]),
                  "fwd": {"kernel_ms": seg_ms["fwd"], "achieved": f_fwd / (seg_ms["fwd"] / 1000) / 1e12,
                          "frac": f_fwd / (seg_ms["fwd"] / 1000) / 1e12 / peak},
@@ -433,8 +433,8 @@ class Workload:
             ach = nbytes / (seg_ms["fwd"] / 1000) / 1e9
             return {"bound": "hbm", "kernel": "sig_fwd_stream_kernel + logsig_fwd_t_kernel (stream logsignature, "
                     "bytes of both kernels)", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs", "kernel_ms": seg_ms["fwd"],
-                    "output_gbs": rows * self.W * 4 / (seg_ms["fwd"] / 1000) / 1e9}
+                    "traffic": traffic.get("dominant_kernel"), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "kernel_ms": seg_ms["fwd"], "output_gbs": rows * self.W * 4 / (seg_ms["fwd"] / 1000) / 1e9}
         if op == "sig_fwd_stream":
             hbm = 6543.7
             try:
@@ -445,14 +445,14 @@ class Workload:
             ach = nbytes / (seg_ms["fwd"] / 1000) / 1e9
             return {"bound": "hbm", "kernel": "sig_fwd_stream_kernel (stream=True, staged rows + TMA bulk stores)",
                     "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": traffic.get("sig_fwd_kernel"), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "traffic": traffic.get("dominant_kernel"), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "kernel_ms": seg_ms["fwd"]}
         f = alg_flops("fwd", B, M, C, N)
         ach = f / (seg_ms["fwd"] / 1000) / 1e12
         r = {"bound": "alu",
              "kernel": "sig_fwd_kernel (+ ordered chunk fold" + (", NCCL all-gather)" if self.world > 1 else ")"),
              "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-             "traffic": traffic.get("sig_fwd_kernel"), "peak_source": peak_src, "kernel_ms": seg_ms["fwd"]}
+             "traffic": traffic.get("dominant_kernel"), "peak_source": peak_src, "kernel_ms": seg_ms["fwd"]}
         r.update(meas(ach))
         return r
 
