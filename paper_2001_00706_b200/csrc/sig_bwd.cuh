@@ -108,6 +108,20 @@ __device__ __forceinline__ void stage_path_increments(const BwdParams& prm, int6
 #define SIG_BWD_STAGGER 400
 #endif
 
+#ifndef SIG_BWD_GNS
+#define SIG_BWD_GNS 0
+#endif
+#ifndef SIG_BWD_GNS_MAXKB
+#define SIG_BWD_GNS_MAXKB 96
+#endif
+#ifndef SIG_BWD_GNS_MINB
+#define SIG_BWD_GNS_MINB 2
+#endif
+// Dot products over channels in vjp_visit as scalar FFMA chains (no horizontal add per node) or as
+// FFMA2 on channel pairs plus one FADD.
+#ifndef SIG_BWD_SDOT
+#define SIG_BWD_SDOT 0
+#endif
 template <class SH>
 struct BwdLayout {
     static constexpr int C = SH::C, N = SH::N, P = SH::P;
@@ -121,7 +135,14 @@ struct BwdLayout {
     static constexpr int REC = C;
     // one-warp CTAs (e.g. C=3, N=6 with 27 prefixes) run as time chunks of long paths: ask for 16
     // resident per SM (<= 128 registers), the latency of one warp's reversal hidden by the others
-    static constexpr int MINB = (NT == 32 && SH::OWN + SH::OWNA <= 64) ? 16 : 1;
+    // GNS: the constant top-level gradient G_N lives in shared memory, not in registers (each
+    // thread's block of C^(N-P) floats stored as float4 columns, [j/4][thread][4], conflict-free):
+    // frees C^(N-P) registers per thread so that two CTAs fit per SM (plain and chunked calls,
+    // not stream mode).  Each G_N value feeds two FMAs per step (gz and beta), one LDS.128 per four.
+    static constexpr bool GNS = SIG_BWD_GNS && (C % 4 == 0) && (SH::own(N) >= 16) && (SH::CP % 32 == 0) &&
+                                (SH::P > 0) && ((size_t)NT * SH::own(N) * 4 <= SIG_BWD_GNS_MAXKB * 1024);
+    static constexpr int GNF = GNS ? NT * SH::own(N) : 0;  // floats of the G_N region
+    static constexpr int MINB = (NT == 32 && SH::OWN + SH::OWNA <= 64) ? 16 : (GNS ? SIG_BWD_GNS_MINB : 1);
     static constexpr int RECS = FAST ? HW : NT;      // records per step
     // shared memory of a tile of T steps: the tile's increments, T + 1 record slots, the per-step
     // totals, gprev, and the low-level partials of grad_initial
@@ -142,34 +163,54 @@ struct BwdLayout {
 // (s = K-I), after adding the level-(I+1) gz contributions (1/s) B_I[p.W] beta_{I+1}[p.W.c] and
 // G_I += beta_I for owned levels I < K.  The leaves are beta_K = G_K (read before any chain
 // k' > K adds into it: chains run bottom-up).
-template <class SH, int K, int I, int W, int SA>
+// GNS (top chain only): the leaves G_N[p.W.c] come from shared memory, gns = the thread's column
+// (element j of its block at gns[(j/4) * 4 NT + j%4]).
+template <class SH, int K, int I, int W, int SA, bool GNS = false>
 __device__ __forceinline__ float vjp_visit(float BI, float (&G)[SH::OWN], const float (&A)[SA], const float (&z)[SH::C],
-                                           float (&gz)[SH::C]) {
+                                           float (&gz)[SH::C], const float* gns = nullptr) {
     // channel pairs with the packed FFMA2 (see horner_visit): gz += bs * x and acc += x * z
     constexpr int C = SH::C;
     constexpr float sc = inv_int(K - I);
     const float bs = BI * sc;
     const float2 bs2 = make_float2(bs, bs);
     float2 acc2 = make_float2(0.0f, 0.0f);
+    float gl[(GNS && I + 1 == K) ? C : 1];
+    if constexpr (GNS && I + 1 == K) {
+        static_for<0, C / 4>([&](auto qq) {
+            constexpr int q = decltype(qq)::value;
+            constexpr int j = W * C + 4 * q;
+            const float4 v = *reinterpret_cast<const float4*>(gns + (j / 4) * (4 * BwdLayout<SH>::NT));
+            gl[4 * q] = v.x;
+            gl[4 * q + 1] = v.y;
+            gl[4 * q + 2] = v.z;
+            gl[4 * q + 3] = v.w;
+        });
+    }
     static_for<0, C / 2>([&](auto cc) {
         constexpr int c = 2 * decltype(cc)::value;
         constexpr int ch = W * C + c;
         const float2 z2 = make_float2(z[c], z[c + 1]);
         float2 x;
         if constexpr (I + 1 == K) {
-            x = make_float2(G[SH::own_off(K) + ch], G[SH::own_off(K) + ch + 1]);
+            if constexpr (GNS) x = make_float2(gl[c], gl[c + 1]);
+            else x = make_float2(G[SH::own_off(K) + ch], G[SH::own_off(K) + ch + 1]);
         } else {
             constexpr int o = SH::own_off(I + 1) + ch;
             const float2 Bc = __ffma2_rn(bs2, z2, make_float2(A[o], A[o + 1]));
-            x.x = vjp_visit<SH, K, I + 1, ch>(Bc.x, G, A, z, gz);
-            x.y = vjp_visit<SH, K, I + 1, ch + 1>(Bc.y, G, A, z, gz);
+            x.x = vjp_visit<SH, K, I + 1, ch, SA, GNS>(Bc.x, G, A, z, gz, gns);
+            x.y = vjp_visit<SH, K, I + 1, ch + 1, SA, GNS>(Bc.y, G, A, z, gz, gns);
         }
         const float2 g2 = __ffma2_rn(bs2, x, make_float2(gz[c], gz[c + 1]));
         gz[c] = g2.x;
         gz[c + 1] = g2.y;
-        acc2 = __ffma2_rn(x, z2, acc2);
+        if constexpr (SIG_BWD_SDOT) {
+            acc2.x = fmaf(x.x, z2.x, acc2.x);
+            acc2.x = fmaf(x.y, z2.y, acc2.x);
+        } else {
+            acc2 = __ffma2_rn(x, z2, acc2);
+        }
     });
-    float acc = acc2.x + acc2.y;
+    float acc = SIG_BWD_SDOT ? acc2.x : acc2.x + acc2.y;
     if constexpr (C % 2 == 1) {
         constexpr int c = C - 1;
         constexpr int ch = W * C + c;
@@ -329,7 +370,10 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, BwdLayout<SH>::MINB) sig_bw
     constexpr int C = SH::C, N = SH::N, P = SH::P;
     constexpr int HW = LY::HW;
     constexpr int64_t S = SH::S;
-    extern __shared__ __align__(16) float sm[];
+    extern __shared__ __align__(16) float sm_base[];
+    constexpr bool GNS = LY::GNS && !STREAM;
+    float* const gn = sm_base;                                   // GNS: [own(N)/4][NT][4] G_N columns
+    float* const sm = sm_base + (GNS ? LY::GNF : 0);
     const int64_t unit = blockIdx.x;
     const int64_t bidx = unit / prm.n_chunks;            // path
     const int64_t jc = unit - bidx * prm.n_chunks;       // time chunk
@@ -374,9 +418,24 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, BwdLayout<SH>::MINB) sig_bw
         constexpr int k = decltype(kc)::value;
         load_run<SH::own(k), SH::own_off(k)>(A, sigrow + SH::lvl_off(k) + (int64_t)prefix * SH::own(k));
     });
+    const float* gns = gn + 4 * tid;
     static_for<SH::K0, N + 1>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        if (STREAM || !valid) {
+        if constexpr (GNS && k == N) {
+            // the thread's own column: written and read by this thread only (no barrier needed)
+            float tmp[SH::own(N)];
+            if (valid) {
+                load_run<SH::own(N), 0>(tmp, prm.grad_out + (size_t)unit * prm.go_stride + SH::lvl_off(N) +
+                                                 (int64_t)prefix * SH::own(N));
+            } else {
+#pragma unroll
+                for (int q = 0; q < SH::own(N); ++q) tmp[q] = 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < SH::own(N) / 4; ++q)
+                *reinterpret_cast<float4*>(gn + q * 4 * LY::NT + 4 * tid) =
+                    make_float4(tmp[4 * q], tmp[4 * q + 1], tmp[4 * q + 2], tmp[4 * q + 3]);
+        } else if (STREAM || !valid) {
 #pragma unroll
             for (int q = 0; q < SH::own(k); ++q) G[SH::own_off(k) + q] = 0.0f;
         } else {
@@ -481,7 +540,7 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, BwdLayout<SH>::MINB) sig_bw
         prefix_chain_all<SH, k>(Bp, A, low, zp);
         float bP;
         if constexpr (k == P) bP = G[SH::own_off(P)];
-        else bP = vjp_visit<SH, k, P, 0>(Bp[P], G, A, z, gz);
+        else bP = vjp_visit<SH, k, P, 0, SH::OWNA, GNS>(Bp[P], G, A, z, gz, gns);
         if constexpr (P >= 1) low_tail<SH, k, P>(bP, Bp, zp, acc, Gh);
     };
 
@@ -646,7 +705,20 @@ __global__ void __launch_bounds__(BwdLayout<SH>::NT, BwdLayout<SH>::MINB) sig_bw
         if (valid) {
             static_for<SH::K0, N + 1>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                store_run<SH::own(k), SH::own_off(k), false>(gi + SH::lvl_off(k) + (int64_t)prefix * SH::own(k), G);
+                if constexpr (GNS && k == N) {
+                    float tmp[SH::own(N)];
+#pragma unroll
+                    for (int q = 0; q < SH::own(N) / 4; ++q) {
+                        const float4 v = *reinterpret_cast<const float4*>(gn + q * 4 * LY::NT + 4 * tid);
+                        tmp[4 * q] = v.x;
+                        tmp[4 * q + 1] = v.y;
+                        tmp[4 * q + 2] = v.z;
+                        tmp[4 * q + 3] = v.w;
+                    }
+                    store_run<SH::own(N), 0, false>(gi + SH::lvl_off(N) + (int64_t)prefix * SH::own(N), tmp);
+                } else {
+                    store_run<SH::own(k), SH::own_off(k), false>(gi + SH::lvl_off(k) + (int64_t)prefix * SH::own(k), G);
+                }
             });
         }
         static_for<1, P>([&](auto ic) {
@@ -1325,9 +1397,11 @@ cudaError_t launch_bwd(const BwdParams& prm, cudaStream_t st) {
     // backward: 1-warp CTAs, 16 per SM), at most SIG_BWD_TILE_KB
     size_t budget = (size_t)228 * 1024 / slots - 1024;
     if (budget > (size_t)SIG_BWD_TILE_KB * 1024) budget = (size_t)SIG_BWD_TILE_KB * 1024;
+    const size_t gnb = prm.stream ? 0 : (size_t)LY::GNF * sizeof(float);  // GNS region (plain kernel)
+    budget = budget > gnb + 4096 ? budget - gnb : 4096;
     BwdParams q = prm;
     q.tile = LY::tile(prm.chunk_len, budget);
-    const size_t smem = LY::smem_bytes_tile(q.tile);
+    const size_t smem = LY::smem_bytes_tile(q.tile) + gnb;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
