@@ -113,6 +113,35 @@ sig_status_t sig_signature_backward(const float* grad_out, const float* path, co
                                     const float* basepoint, float* grad_path, float* grad_basepoint,
                                     sig_cuda_stream_t s);
 
+/* ---------------------------------------------------------------- forward with saved chunk states */
+
+/* The time-parallel backward (sig_signature_backward_ex with workspace; Chen's
+ * identity P:L84-87 over time chunks) starts chunk j's reversal (eq-reverse)
+ * from the product of the chunks before it and needs the products after it for the chunk-end
+ * gradients; without saved state it recomputes every chunk's signature (one forward pass over the
+ * whole path) first.  This pair keeps them instead: sig_signature_save computes the chunk
+ * signatures S_j and their inclusive prefix products P_{j+1} = S_0 [x] .. [x] S_j (the signature
+ * is the last one, copied to `out`), and sig_signature_backward_saved reverses every chunk in
+ * parallel from them.  Plain calls only (no stream, inverse or initial).  When the batch fills the
+ * GPU without chunks (sig_signature_saved_bytes(...) == 0) both are the plain forward / reversal.
+ *   saved  device buffer of sig_signature_saved_bytes(...) bytes: [2][B, m, S] floats, m chunks;
+ *          written by sig_signature_save, read by sig_signature_backward_saved for the SAME path,
+ *          B, L, C, depth and basepoint (not checked); owned by the caller
+ *   ws     sig_signature_save_workspace_size(...) resp. sig_signature_backward_saved_workspace_size
+ *          bytes (scan scratch; suffix products, chunk-end gradients and the shared-point buffer)
+ * Errors: as sig_signature / sig_signature_backward; WORKSPACE when saved or ws is too small. */
+size_t sig_signature_saved_bytes(int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp);
+size_t sig_signature_save_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp);
+sig_status_t sig_signature_save(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp,
+                                const float* basepoint, float* out, float* saved, size_t saved_bytes, void* ws,
+                                size_t ws_bytes, sig_cuda_stream_t s);
+size_t sig_signature_backward_saved_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth,
+                                                   sig_basepoint_t bp);
+sig_status_t sig_signature_backward_saved(const float* grad_out, const float* path, const float* out_saved,
+                                          const float* saved, size_t saved_bytes, int64_t B, int64_t L, int64_t C,
+                                          int32_t depth, sig_basepoint_t bp, const float* basepoint, float* grad_path,
+                                          float* grad_basepoint, void* ws, size_t ws_bytes, sig_cuda_stream_t s);
+
 /* ---------------------------------------------------------------- host-resident batches */
 
 /* Signature forward + reversible backward of a batch that lives in HOST memory (the training step

@@ -24,7 +24,8 @@ import torch
 __all__ = [
     "lib", "LIB_PATH", "SigError",
     "sig_signature_channels", "sig_logsignature_channels", "sig_is_supported",
-    "sig_signature", "sig_signature_backward", "sig_signature_combine", "sig_signature_combine_backward",
+    "sig_signature", "sig_signature_backward", "sig_signature_save", "sig_signature_backward_saved",
+    "sig_signature_combine", "sig_signature_combine_backward",
     "sig_multi_signature_combine", "LogSigPlan", "sig_logsignature", "sig_logsignature_backward",
     "signature", "logsignature", "signature_combine", "multi_signature_combine",
     "BP_NONE", "BP_ZERO", "BP_GIVEN", "MODES",
@@ -78,6 +79,15 @@ def lib():
                 ("sig_signature_backward_ex", ctypes.c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _c_i32,
                                                              ctypes.c_int, _vp, _c_i32, _vp, _vp, _vp, _vp, _vp,
                                                              _c_sz, _vp]),
+                ("sig_signature_saved_bytes", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, ctypes.c_int]),
+                ("sig_signature_save_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, ctypes.c_int]),
+                ("sig_signature_save", ctypes.c_int, [_vp, _c_i64, _c_i64, _c_i64, _c_i32, ctypes.c_int, _vp, _vp,
+                                                      _vp, _c_sz, _vp, _c_sz, _vp]),
+                ("sig_signature_backward_saved_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32,
+                                                                        ctypes.c_int]),
+                ("sig_signature_backward_saved", ctypes.c_int, [_vp, _vp, _vp, _vp, _c_sz, _c_i64, _c_i64, _c_i64,
+                                                                _c_i32, ctypes.c_int, _vp, _vp, _vp, _vp, _c_sz,
+                                                                _vp]),
                 ("sig_signature_fwd_bwd_host_workspace_size", _c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32]),
                 ("sig_signature_fwd_bwd_host", ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i32, _vp, _c_i32,
                                                               _vp, _c_sz, _vp]),
@@ -264,6 +274,56 @@ def sig_signature_backward_ex(grad_out, path, out_saved, depth: int, stream: boo
     return gp, gbp, gi
 
 
+@_on_device
+def sig_signature_save(path, depth: int, basepoint=None):
+    """sig_signature_save: the signature plus the chunk states the time-parallel backward starts
+    from (include/sig.h) -> (out [B, S], saved uint8 tensor or None when the backward would not
+    chunk).  Pass both to sig_signature_backward_saved."""
+    path = _dev_f32(path, "path")
+    B, L, C = _path3(path)
+    bpm, bp = _bp(basepoint, path)
+    Lib = lib()
+    S = Lib.sig_signature_channels(C, depth)
+    if S < 0:
+        raise SigError(f"bad C={C} depth={depth}")
+    out = torch.empty((B, S), device=path.device, dtype=torch.float32)
+    sb = Lib.sig_signature_saved_bytes(B, L, C, depth, bpm)
+    saved = torch.empty(sb, device=path.device, dtype=torch.uint8) if sb else None
+    wsb = Lib.sig_signature_save_workspace_size(B, L, C, depth, bpm)
+    ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_signature_save(_ptr(path), B, L, C, depth, bpm, _ptr(bp), _ptr(out), _ptr(saved), sb, _ptr(ws),
+                                  wsb, _stream(path.device)), "sig_signature_save")
+    return out, saved
+
+
+@_on_device
+def sig_signature_backward_saved(grad_out, path, out_saved, saved, depth: int, basepoint=None):
+    """sig_signature_backward_saved -> (grad_path, grad_basepoint or None)."""
+    path = _dev_f32(path, "path")
+    grad_out = _dev_f32(grad_out, "grad_out")
+    out_saved = _dev_f32(out_saved, "out_saved")
+    B, L, C = _path3(path)
+    bpm, bp = _bp(basepoint, path)
+    Lib = lib()
+    S = Lib.sig_signature_channels(C, depth)
+    if S < 0:
+        raise SigError(f"bad C={C} depth={depth}")
+    _shape(grad_out, (B, S), "grad_out")
+    _shape(out_saved, (B, S), "out_saved")
+    sb = Lib.sig_signature_saved_bytes(B, L, C, depth, bpm)
+    if sb and (saved is None or saved.numel() < sb or saved.device != path.device):
+        raise SigError(f"saved must be the {sb}-byte tensor sig_signature_save returned for this call")
+    gp = torch.empty_like(path)
+    gbp = torch.empty((B, C), device=path.device, dtype=torch.float32) if bpm == BP_GIVEN else None
+    wsb = Lib.sig_signature_backward_saved_workspace_size(B, L, C, depth, bpm)
+    ws = torch.empty(wsb, device=path.device, dtype=torch.uint8) if wsb else None
+    _check(Lib.sig_signature_backward_saved(_ptr(grad_out), _ptr(path), _ptr(out_saved),
+                                            _ptr(saved) if sb else None, sb, B, L, C, depth, bpm, _ptr(bp),
+                                            _ptr(gp), _ptr(gbp), _ptr(ws), wsb, _stream(path.device)),
+           "sig_signature_backward_saved")
+    return gp, gbp
+
+
 def sig_signature_fwd_bwd_host(path_h, grad_out_h, depth: int, chunks: int = 4, grad_path_h=None, device=None):
     """sig_signature_fwd_bwd_host: forward + reversible backward of a HOST-resident batch, in
     `chunks` slices whose copies overlap the kernels (include/sig.h).  path_h [B, L, C] and
@@ -407,7 +467,13 @@ class _Signature(torch.autograd.Function):
     @staticmethod
     def forward(ctx, path, depth, stream, basepoint_flag, bp_tensor, inverse, initial):
         bp = bp_tensor if basepoint_flag == BP_GIVEN else (basepoint_flag == BP_ZERO)
-        out = sig_signature(path, depth, stream, bp, inverse=inverse, initial=initial)
+        ctx.chunks = None
+        if not stream and not inverse and initial is None and ctx.needs_input_grad[0]:
+            # a backward will follow: keep the chunk states its time-parallel reversal starts from
+            # (None when the batch fills the GPU without chunks)
+            out, ctx.chunks = sig_signature_save(path, depth, bp)
+        else:
+            out = sig_signature(path, depth, stream, bp, inverse=inverse, initial=initial)
         ctx.save_for_backward(path, out, bp_tensor if basepoint_flag == BP_GIVEN else None, initial)
         ctx.depth, ctx.stream, ctx.bpf, ctx.inverse = depth, stream, basepoint_flag, inverse
         return out
@@ -416,6 +482,10 @@ class _Signature(torch.autograd.Function):
     def backward(ctx, grad_out):
         path, out, bpt, initial = ctx.saved_tensors
         bp = bpt if ctx.bpf == BP_GIVEN else (ctx.bpf == BP_ZERO)
+        if ctx.chunks is not None:
+            gp, gbp = sig_signature_backward_saved(grad_out.contiguous(), path, out, ctx.chunks, ctx.depth, bp)
+            ctx.chunks = None
+            return gp, None, None, None, gbp, None, None
         if not ctx.inverse and initial is None:
             gp, gbp = sig_signature_backward(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp)
             return gp, None, None, None, gbp, None, None

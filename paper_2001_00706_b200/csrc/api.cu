@@ -485,37 +485,62 @@ cudaError_t chunk_scan(const TensorDims& d, ScanLaunch sc, const float* in, floa
 // prefix and suffix products (K3 steps), the gradient at the end of every chunk, then reverse all
 // chunks at once (K2, one CTA per chunk, each starting from its prefix product) and add the shares
 // of the points two chunks have in common.
-sig_status_t run_bwd_chunked(const FwdPlan& pl, const BwdChunking& ch, BwdParams prm, const TensorDims& d, void* ws,
-                             cudaStream_t s) {
-    const int64_t B = prm.B, m = ch.m, S = d.S, C = d.C;
-    const size_t rows = (size_t)B * m;
-    float* units = static_cast<float*>(ws);
-    float* pin = units + rows * S;
-    float* sfx = pin + rows * S;
-    float* tmp = sfx + rows * S;
-    float* gend = tmp + rows * S;
-    float* edge = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align256(5 * rows * (size_t)S * sizeof(float)));
+// Chunk signatures S_j of every path ([B, m, S], unit u = chunk u mod m of path u / m) by one K1
+// launch over all chunks (the same launch for the forward's saved state and the backward's
+// recomputation, so both produce the same bits).
+cudaError_t launch_chunk_sigs(const FwdPlan& pl, const BwdChunking& ch, const BwdParams& prm, const TensorDims& d,
+                              float* units, cudaStream_t s) {
     FwdParams f{};
     f.path = prm.path;
     f.basepoint = prm.basepoint;
     f.bp_mode = prm.bp_mode;
     f.stream = 0;
-    f.B = B;
+    f.B = prm.B;
     f.L = prm.L;
     f.M = pl.M;
     f.chunk_len = ch.chunk_len;
-    f.n_chunks = m;
-    f.n_units = (int64_t)rows;
+    f.n_chunks = ch.m;
+    f.n_units = prm.B * ch.m;
     f.upc = 0;
     f.dims = d;
     f.out = units;
     f.zsign = prm.zsign;
     f.initial = prm.initial;
     cudaError_t e = pl.ks->fwd0(f, s);
-    if (e != cudaSuccess) return cuda_status(e, "chunk signature launch");
-    count_launch();
-    e = chunk_scan(d, pl.ks->scan, units, pin, tmp, B, m, 0, s);
-    if (e == cudaSuccess) e = chunk_scan(d, pl.ks->scan, units, sfx, tmp, B, m, 1, s);
+    if (e == cudaSuccess) count_launch();
+    return e;
+}
+
+// saved: the forward's chunk signatures and their inclusive prefix products ([2][B, m, S], from
+// sig_signature_save), or nullptr to recompute them here.
+sig_status_t run_bwd_chunked(const FwdPlan& pl, const BwdChunking& ch, BwdParams prm, const TensorDims& d, void* ws,
+                             cudaStream_t s, const float* saved = nullptr) {
+    const int64_t B = prm.B, m = ch.m, S = d.S, C = d.C;
+    const size_t rows = (size_t)B * m;
+    float* w = static_cast<float*>(ws);
+    const float* units;
+    const float* pin;
+    cudaError_t e = cudaSuccess;
+    if (saved) {
+        units = saved;
+        pin = saved + rows * S;
+    } else {
+        float* u = w;
+        float* pn = u + rows * S;
+        w = pn + rows * S;
+        e = launch_chunk_sigs(pl, ch, prm, d, u, s);
+        if (e != cudaSuccess) return cuda_status(e, "chunk signature launch");
+        e = chunk_scan(d, pl.ks->scan, u, pn, w + rows * S, B, m, 0, s);
+        if (e != cudaSuccess) return cuda_status(e, "chunk scan launch");
+        units = u;
+        pin = pn;
+    }
+    float* sfx = w;
+    float* tmp = sfx + rows * S;
+    float* gend = tmp + rows * S;
+    float* edge = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
+                                           align256((saved ? 3 : 5) * rows * (size_t)S * sizeof(float)));
+    e = chunk_scan(d, pl.ks->scan, units, sfx, tmp, B, m, 1, s);
     if (e != cudaSuccess) return cuda_status(e, "chunk scan launch");
     const int64_t n = (int64_t)rows * S;
     chunk_gend_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, prm.grad_out, sfx, B, m, gend);
@@ -831,6 +856,109 @@ sig_status_t sig_signature_backward_ex(const float* grad_out, const float* path,
         if (e != cudaSuccess) return cuda_status(e, "word reversal launch");
     }
     return ok();
+}
+
+// ---------------------------------------------------------------- saved chunk states
+// (sig.h "forward with saved chunk states"): the time-parallel backward starts every chunk from the
+// product of the earlier chunks; the forward can leave those states behind instead of the backward
+// recomputing them (one K1 pass over the whole path plus a prefix scan).
+// chunking of the backward for a plain call (no stream / inverse / initial); m <= 1: none
+static bool saved_plan(int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp, FwdPlan& pl, BwdChunking& ch) {
+    if (make_fwd_plan(B, L, C, depth, 0, bp, pl) != SIG_OK || !pl.ks->bwd || B <= 0) return false;
+    bwd_chunking(pl, B, 0, true, ch);
+    return ch.m > 1;
+}
+
+size_t sig_signature_saved_bytes(int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp) {
+    FwdPlan pl;
+    BwdChunking ch;
+    if (!saved_plan(B, L, C, depth, bp, pl, ch)) return 0;
+    return align256(2 * (size_t)B * ch.m * (size_t)sig_channels_checked(C, depth) * sizeof(float));
+}
+
+size_t sig_signature_save_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp) {
+    FwdPlan pl;
+    BwdChunking ch;
+    if (!saved_plan(B, L, C, depth, bp, pl, ch)) return sig_signature_workspace_size(B, L, C, depth, 0, bp);
+    return align256((size_t)B * ch.m * (size_t)sig_channels_checked(C, depth) * sizeof(float));
+}
+
+sig_status_t sig_signature_save(const float* path, int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp,
+                                const float* basepoint, float* out, float* saved, size_t saved_bytes, void* ws,
+                                size_t ws_bytes, sig_cuda_stream_t s) {
+    FwdPlan pl;
+    BwdChunking ch;
+    if (!saved_plan(B, L, C, depth, bp, pl, ch))  // no chunks: the plain forward (argument checks there)
+        return run_signature(path, B, L, C, depth, 0, bp, basepoint, out, ws, ws_bytes, (cudaStream_t)s);
+    if (!path || !out || !saved) return fail(SIG_ERR_INVALID_ARG, "path, out and saved must be non-null");
+    if (bp == SIG_BP_GIVEN && !basepoint) return fail(SIG_ERR_INVALID_ARG, "basepoint is NULL with SIG_BP_GIVEN");
+    const size_t need_saved = sig_signature_saved_bytes(B, L, C, depth, bp);
+    const size_t need_ws = sig_signature_save_workspace_size(B, L, C, depth, bp);
+    if (saved_bytes < need_saved)
+        return fail(SIG_ERR_WORKSPACE, "saved buffer of %zu bytes needed, %zu given", need_saved, saved_bytes);
+    if (ws_bytes < need_ws || !ws) return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need_ws, ws_bytes);
+    const TensorDims d = make_dims((int)C, depth);
+    const int64_t S = d.S, m = ch.m;
+    const size_t rows = (size_t)B * m;
+    BwdParams prm{};
+    prm.path = path;
+    prm.basepoint = basepoint;
+    prm.bp_mode = (int)bp;
+    prm.B = B;
+    prm.L = L;
+    prm.M = pl.M;
+    prm.zsign = 1.0f;
+    cudaStream_t cs = (cudaStream_t)s;
+    cudaError_t e = launch_chunk_sigs(pl, ch, prm, d, saved, cs);
+    if (e != cudaSuccess) return cuda_status(e, "chunk signature launch");
+    float* pin = saved + rows * S;  // inclusive prefix products: the last one of a path is its signature
+    e = chunk_scan(d, pl.ks->scan, saved, pin, static_cast<float*>(ws), B, m, 0, cs);
+    if (e != cudaSuccess) return cuda_status(e, "chunk scan launch");
+    e = cudaMemcpy2DAsync(out, (size_t)S * sizeof(float), pin + (size_t)(m - 1) * S, (size_t)m * S * sizeof(float),
+                          (size_t)S * sizeof(float), (size_t)B, cudaMemcpyDeviceToDevice, cs);
+    return cuda_status(e, "signature copy");
+}
+
+size_t sig_signature_backward_saved_workspace_size(int64_t B, int64_t L, int64_t C, int32_t depth, sig_basepoint_t bp) {
+    FwdPlan pl;
+    BwdChunking ch;
+    if (!saved_plan(B, L, C, depth, bp, pl, ch)) return 0;
+    const size_t S = (size_t)sig_channels_checked(C, depth), rows = (size_t)B * ch.m;
+    return align256(3 * rows * S * sizeof(float)) + align256(rows * (size_t)C * sizeof(float));
+}
+
+sig_status_t sig_signature_backward_saved(const float* grad_out, const float* path, const float* out_saved,
+                                          const float* saved, size_t saved_bytes, int64_t B, int64_t L, int64_t C,
+                                          int32_t depth, sig_basepoint_t bp, const float* basepoint, float* grad_path,
+                                          float* grad_basepoint, void* ws, size_t ws_bytes, sig_cuda_stream_t s) {
+    FwdPlan pl;
+    BwdChunking ch;
+    if (!saved_plan(B, L, C, depth, bp, pl, ch))  // no chunks: the plain reversal from out_saved
+        return sig_signature_backward_ex(grad_out, path, out_saved, B, L, C, depth, 0, bp, basepoint, 0, nullptr,
+                                         grad_path, grad_basepoint, nullptr, nullptr, 0, s);
+    if (!grad_out || !path || !saved || !grad_path)
+        return fail(SIG_ERR_INVALID_ARG, "grad_out, path, saved and grad_path must be non-null");
+    if (bp == SIG_BP_GIVEN && !basepoint) return fail(SIG_ERR_INVALID_ARG, "basepoint is NULL with SIG_BP_GIVEN");
+    const size_t need_saved = sig_signature_saved_bytes(B, L, C, depth, bp);
+    const size_t need_ws = sig_signature_backward_saved_workspace_size(B, L, C, depth, bp);
+    if (saved_bytes < need_saved)
+        return fail(SIG_ERR_WORKSPACE, "saved buffer of %zu bytes needed, %zu given", need_saved, saved_bytes);
+    if (ws_bytes < need_ws || !ws) return fail(SIG_ERR_WORKSPACE, "workspace of %zu bytes needed, %zu given", need_ws, ws_bytes);
+    const TensorDims d = make_dims((int)C, depth);
+    BwdParams prm{};
+    prm.grad_out = grad_out;
+    prm.path = path;
+    prm.basepoint = basepoint;
+    prm.bp_mode = (int)bp;
+    prm.stream = 0;
+    prm.B = B;
+    prm.L = L;
+    prm.M = pl.M;
+    prm.grad_path = grad_path;
+    prm.grad_bp = (bp == SIG_BP_GIVEN) ? grad_basepoint : nullptr;
+    prm.zsign = 1.0f;
+    prm.go_stride = d.S;
+    return run_bwd_chunked(pl, ch, prm, d, ws, (cudaStream_t)s, saved);
 }
 
 sig_status_t sig_signature_backward(const float* grad_out, const float* path, const float* out_saved, int64_t B,
