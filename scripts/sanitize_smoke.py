@@ -43,5 +43,8 @@ gp7 = torch.empty_like(x7)
 Lib = sb.lib()
 assert Lib.sig_signature_backward(sb._ptr(g7), sb._ptr(x7), sb._ptr(s7), 1, 20000, 3, 6, 0, sb.BP_NONE, None,
                                   sb._ptr(gp7), None, sb._stream(x7.device)) == 0
+# round 2: forward with saved chunk states and the backward that starts from them
+o8, sv8 = sb.sig_signature_save(x7, 6)
+sb.sig_signature_backward_saved(g7, x7, o8, sv8, 6)
 torch.cuda.synchronize()
 print("ok")
