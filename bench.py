@@ -629,6 +629,67 @@ def measure_e2e(wl, steps: int, world: int, dev):
                       "copies overlap the kernels" if wl.pipe is not None else ""))}
 
 
+def measure_e2e_train(wl, steps: int, world: int, dev):
+    """The fwd + bwd step as a training step through the public autograd API: per step the batch of
+    paths goes host -> device (pinned), out = signature(x), loss = <W, out> with W [S] a
+    device-resident linear head, loss.backward() (the reversible backward kernels), and the loss
+    comes back device -> host.  The upstream gradient is produced on the device, as in training;
+    `e2e` (above) is the stricter variant that also ships a [B, S] upstream gradient from the host."""
+    import torch
+
+    sb, N = wl.sb, wl.N
+    stream = wl.stream
+    xh = torch.from_numpy(wl.x_np).pin_memory()
+    xd = [torch.empty(xh.shape, dtype=torch.float32, device=dev) for _ in range(2)]
+    W = torch.from_numpy(normal((wl.S,), 4242)).to(dev)
+    lossh = torch.empty((), dtype=torch.float32).pin_memory()
+    # a data loader's double buffering: the next batch's H2D runs on a copy stream while this batch
+    # computes (every batch is still copied inside the timed region)
+    cstream = torch.cuda.Stream(dev)
+    arrived = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    it = [0]
+
+    def load(k):
+        with torch.cuda.stream(cstream):
+            cstream.wait_event(consumed[k])
+            xd[k].copy_(xh, non_blocking=True)
+            arrived[k].record(cstream)
+
+    def step():
+        k = it[0] % 2
+        load(1 - k)  # the next batch
+        stream.wait_event(arrived[k])
+        x = xd[k].detach().requires_grad_(True)
+        loss = (sb.signature(x, N) @ W).sum()
+        loss.backward()
+        consumed[k].record(stream)
+        lossh.copy_(loss.detach(), non_blocking=True)
+        it[0] += 1
+
+    for ev_ in consumed:
+        ev_.record(stream)
+    load(0)
+
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize(dev)
+    _barrier(world)
+    n = max(3, min(steps, 50))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    e_ms = _max_over_ranks(a.elapsed_time(b) / n, world, dev)
+    units = _sum_over_ranks(wl.units, world, dev)
+    return {"value": units / (e_ms / 1000), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
+            "d2h_bytes_per_step": 4,
+            "path": "autograd: signature(x) -> loss = <W, Sig> (W [S] on the device) -> loss.backward(); "
+                    "paths H2D (double-buffered on a copy stream) and the loss D2H every step"}
+
+
 def _metric_name(name):
     return METRIC if name == "c2" else f"{CONFIGS[name]['op']} paths/sec ({name})"
 
@@ -663,6 +724,7 @@ def run_ours(args, rank: int, world: int):
     value = units / (ms_step / 1000.0)
     roofline = wl.roofline(r["seg_ms"], ms_step)
     e2e = measure_e2e(wl, args.steps, world, dev)
+    e2e_train = measure_e2e_train(wl, args.steps, world, dev) if wl.cfg["op"] == "sig_fwd_bwd" else None
     scaling = wl.scaling
     line = {
         "metric": _metric_name(args.config),
@@ -673,6 +735,8 @@ def run_ours(args, rank: int, world: int):
         "config": _config_dict(args.config, world, scaling, wl.B_global if scaling == "strong" else wl.B, wl.l2),
         "roofline": roofline, "e2e": e2e, "clocks": sampler.summary(), "gpu_launches": r["launches"],
     }
+    if e2e_train is not None:
+        line["e2e_train"] = e2e_train
     del wl
     torch.cuda.empty_cache()
     # the other scaling mode of a batch-sharded config, measured in the same run (at N = 1 both
