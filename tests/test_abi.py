@@ -84,3 +84,27 @@ def test_workspace_query(L):
     assert L.sig_signature_workspace_size(1, 2 ** 22, 3, 6, 0, 0) > 0
     assert L.sig_signature_workspace_size(1024, 128, 8, 5, 0, 0) == 0
     assert L.sig_signature_workspace_size(256, 1024, 6, 4, 1, 0) == 0  # stream mode is never chunked
+
+
+def test_saved_chunk_pair_host_side(L):
+    """sig_signature_save / sig_signature_backward_saved (include/sig.h): sizes are host queries,
+    and missing buffers are rejected before any launch."""
+    # one long path: the backward is time-chunked, so there is state to save ([2][B, m, S] floats)
+    nb = L.sig_signature_saved_bytes(1, 40000, 3, 4, 0)
+    S = 120
+    assert nb >= 2 * 2 * S * 4 and nb % 256 == 0  # at least two chunks, 256-byte rounded
+    assert L.sig_signature_backward_saved_workspace_size(1, 40000, 3, 4, 0) > 0
+    # a batch that fills the GPU is never chunked: nothing to save
+    assert L.sig_signature_saved_bytes(4096, 64, 3, 4, 0) == 0
+    assert L.sig_signature_backward_saved_workspace_size(4096, 64, 3, 4, 0) == 0
+    # stream mode / bad shapes have no saved form
+    assert L.sig_signature_saved_bytes(1, 40000, 9, 3, 0) == 0
+    s = L.sig_signature_save(None, 1, 40000, 3, 4, 0, None, None, None, 0, None, 0, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_INVALID_ARG"
+    p = ctypes.c_void_p(16)
+    s = L.sig_signature_save(p, 1, 40000, 3, 4, 0, None, p, p, 0, p, 1 << 30, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_WORKSPACE"  # saved buffer too small
+    s = L.sig_signature_backward_saved(p, p, p, None, nb, 1, 40000, 3, 4, 0, None, p, None, p, 1 << 30, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_INVALID_ARG"  # saved missing
+    s = L.sig_signature_backward_saved(p, p, p, p, nb - 1, 1, 40000, 3, 4, 0, None, p, None, p, 1 << 30, None)
+    assert L.sig_status_string(s) == b"SIG_ERR_WORKSPACE"
