@@ -180,6 +180,12 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
             int64_t groups = (B * pl.n_chunks + upc - 1) / upc;
             groups = (groups + 147) / 148 * 148;
             int64_t per_path = (groups + B - 1) / B;
+            // a CTA stages its chunks' points and increments at once (2 x upc x chunk x C floats):
+            // keep that within ~110 KB so that two CTAs stay resident per SM (c5: 630-step chunks,
+            // 137 KB, one CTA per SM, 446 us -> 315-step chunks, 68 KB, two per SM, 409 us)
+            while (per_path * upc * 2 <= M / kMinChunk &&
+                   (size_t)2 * upc * ((M + per_path * upc - 1) / (per_path * upc)) * C * sizeof(float) > 110 * 1024)
+                per_path *= 2;
             if (per_path * upc > M) per_path = M / upc > 0 ? M / upc : 1;
             pl.n_chunks = per_path * upc;
         }
