@@ -80,3 +80,41 @@ def test_autograd_uses_saved_chunks():
     gp2, _ = sb.sig_signature_backward(_cuda(g), xt.detach(), out.detach(), N)
     assert torch.equal(xt.grad, gp2)
     assert level_rel_err(out.detach().cpu().numpy(), ref_out.cpu().numpy(), C, N) < FWD_TOL
+
+
+def _random_saved_cases(n=8, seed=2026):
+    rng = np.random.default_rng(seed)
+    shapes = [(2, 6), (2, 9), (3, 4), (3, 6), (4, 4), (4, 5), (5, 3), (6, 3), (7, 3), (8, 3), (8, 4)]
+    out = []
+    while len(out) < n:
+        C, N = shapes[rng.integers(len(shapes))]
+        B = int(rng.integers(1, 9))
+        L = int(rng.integers(600, 6000))
+        bp = [None, "zero", "given"][rng.integers(3)]
+        if sb.lib().sig_signature_saved_bytes(B, L, C, N, {None: 0, "zero": 1, "given": 2}[bp]) > 0:
+            out.append((C, N, B, L, bp))
+    return out
+
+
+@pytest.mark.parametrize("C,N,B,L,bp", _random_saved_cases())
+def test_saved_random_shapes(C, N, B, L, bp):
+    """Seeded random small batches of long paths (chunked backward): the saved pair matches the
+    recomputing backward bit for bit and the oracle within the bars."""
+    x = brownian_paths(B, L, C, seed=C * 100 + N)
+    S = sb.sig_signature_channels(C, N)
+    g = normal((B, S), C + N)
+    bpt = (0.2 * np.random.default_rng(L).standard_normal((B, C))).astype(np.float32) if bp == "given" else None
+    bpa = {None: None, "zero": True, "given": None if bpt is None else _cuda(bpt)}[bp]
+    bpo = {None: None, "zero": True, "given": bpt}[bp]
+    xt, gt = _cuda(x), _cuda(g)
+    out, saved = sb.sig_signature_save(xt, N, basepoint=bpa)
+    gp, gbp = sb.sig_signature_backward_saved(gt, xt, out, saved, N, basepoint=bpa)
+    gp2, gbp2 = sb.sig_signature_backward(gt, xt, out, N, basepoint=bpa)
+    assert torch.equal(gp, gp2)
+    ref = oracle.signature(x, N, basepoint=bpo, threads=8)
+    rg, rbp = oracle.signature_vjp(g, x, N, basepoint=bpo, threads=8)
+    assert level_rel_err(out.cpu().numpy(), ref, C, N) < FWD_TOL
+    assert path_rel_err(gp.cpu().numpy(), rg) < BWD_TOL
+    if bp == "given":
+        assert torch.equal(gbp, gbp2)
+        assert path_rel_err(gbp.cpu().numpy(), rbp) < BWD_TOL
