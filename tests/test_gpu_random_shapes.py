@@ -50,3 +50,44 @@ def test_random_shape_parity(C, N, B, L, bp, stream):
     eb = path_rel_err(gp.cpu().numpy(), rg)
     print(f"PARITY random C={C} N={N} B={B} L={L} bp={bp} stream={stream}: fwd {ef:.2e} bwd {eb:.2e}")
     assert ef < FWD_TOL and eb < BWD_TOL, (ef, eb)
+
+
+def _log_cases(n=18, seed=4242):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        C = int(rng.integers(2, 9))
+        N = int(rng.integers(2, 7))
+        S = sum(C ** k for k in range(1, N + 1))
+        if S > 6000:
+            continue
+        B = int(rng.choice([1, 2, 5, 40]))
+        L = int(rng.choice([2, 6, 33, 150]))
+        if B * (L - 1) * S > 2_000_000:  # oracle budget
+            continue
+        mode = str(rng.choice(["words", "brackets", "expand"]))
+        stream = bool(rng.random() < 0.3) and B * L * S < 400_000
+        bp = str(rng.choice(["none", "zero"]))
+        out.append((C, N, B, L, mode, stream, bp))
+    return out
+
+
+@pytest.mark.parametrize("C,N,B,L,mode,stream,bp", _log_cases())
+def test_random_shape_logsignature(C, N, B, L, mode, stream, bp):
+    """Seeded random shapes through the logsignature (K4 per row / per warp, the three bases) and its
+    backward (K5 into the reversible K2), forward and backward against the float64 oracle."""
+    x = brownian_paths(B, L, C, seed=C * 1000 + N * 100 + L)
+    bpa = True if bp == "zero" else None
+    xt = torch.from_numpy(x).cuda().requires_grad_(True)
+    out = sb.logsignature(xt, N, mode, stream=stream, basepoint=bpa)
+    ref = oracle.logsignature(x, N, mode=mode, stream=stream, basepoint=bpa, threads=8)
+    got = out.detach().cpu().numpy()
+    w = got.shape[-1]
+    den = np.maximum(np.max(np.abs(ref.reshape(-1, w)), axis=1), 1e-30)
+    ef = float(np.max(np.max(np.abs(got.reshape(-1, w) - ref.reshape(-1, w)), axis=1) / den))
+    g = normal(tuple(out.shape), 9)
+    out.backward(torch.from_numpy(g).cuda())
+    rg, _ = oracle.logsignature_vjp(g, x, N, mode=mode, stream=stream, basepoint=bpa, threads=8)
+    eb = path_rel_err(xt.grad.cpu().numpy(), rg)
+    print(f"PARITY random logsig C={C} N={N} B={B} L={L} {mode} stream={stream} bp={bp}: fwd {ef:.2e} bwd {eb:.2e}")
+    assert ef < FWD_TOL and eb < BWD_TOL, (ef, eb)
