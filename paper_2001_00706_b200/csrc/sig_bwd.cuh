@@ -117,10 +117,11 @@ __device__ __forceinline__ void stage_path_increments(const BwdParams& prm, int6
 #ifndef SIG_BWD_GNS_MINB
 #define SIG_BWD_GNS_MINB 2
 #endif
-// Dot products over channels in vjp_visit as scalar FFMA chains (no horizontal add per node) or as
-// FFMA2 on channel pairs plus one FADD.
+// Dot products over channels in vjp_visit as scalar FFMA chains (no horizontal add per node; the
+// default) or as FFMA2 on channel pairs plus one FADD.  Measured (same-run A/B): c5's time-chunked
+// backward (C = 3, odd: pairs + a scalar + the add) 1762 -> 1661 us, c4's backward 683 -> 680 us.
 #ifndef SIG_BWD_SDOT
-#define SIG_BWD_SDOT 0
+#define SIG_BWD_SDOT 1
 #endif
 template <class SH>
 struct BwdLayout {
