@@ -465,10 +465,12 @@ def sig_logsignature_backward(grad_out, path, sig_saved, depth: int, mode: str =
 # ------------------------------------------------------------------------------------------------
 class _Signature(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, path, depth, stream, basepoint_flag, bp_tensor, inverse, initial):
+    def forward(ctx, path, depth, stream, basepoint_flag, bp_tensor, inverse, initial, save):
+        # save: a backward will follow (grad mode on and path requires grad, decided by the caller:
+        # inside forward grad mode is always off)
         bp = bp_tensor if basepoint_flag == BP_GIVEN else (basepoint_flag == BP_ZERO)
         ctx.chunks = None
-        if not stream and not inverse and initial is None and ctx.needs_input_grad[0]:
+        if save and not stream and not inverse and initial is None:
             # a backward will follow: keep the chunk states its time-parallel reversal starts from
             # (None when the batch fills the GPU without chunks)
             out, ctx.chunks = sig_signature_save(path, depth, bp)
@@ -485,14 +487,14 @@ class _Signature(torch.autograd.Function):
         if ctx.chunks is not None:
             gp, gbp = sig_signature_backward_saved(grad_out.contiguous(), path, out, ctx.chunks, ctx.depth, bp)
             ctx.chunks = None
-            return gp, None, None, None, gbp, None, None
+            return gp, None, None, None, gbp, None, None, None
         if not ctx.inverse and initial is None:
             gp, gbp = sig_signature_backward(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp)
-            return gp, None, None, None, gbp, None, None
+            return gp, None, None, None, gbp, None, None, None
         gp, gbp, gi = sig_signature_backward_ex(grad_out.contiguous(), path, out, ctx.depth, ctx.stream, bp,
                                                 inverse=ctx.inverse, initial=initial,
                                                 want_grad_initial=initial is not None and ctx.needs_input_grad[6])
-        return gp, None, None, None, gbp, None, gi
+        return gp, None, None, None, gbp, None, gi, None
 
 
 def _bp_args(basepoint):
@@ -510,7 +512,8 @@ def signature(path: torch.Tensor, depth: int, stream: bool = False, basepoint=No
      -- initial [x] Sig, or Sig^{-1} [x] initial with inverse (reading R18).
     Differentiable in path, basepoint and initial; the backward is the reversible kernel."""
     f, t = _bp_args(basepoint)
-    return _Signature.apply(path, depth, stream, f, t, bool(inverse), initial)
+    save = torch.is_grad_enabled() and path.requires_grad
+    return _Signature.apply(path, depth, stream, f, t, bool(inverse), initial, save)
 
 
 class _LogSignature(torch.autograd.Function):

@@ -75,10 +75,16 @@ def test_autograd_uses_saved_chunks():
     g = normal((B, S), 57)
     xt = _cuda(x).requires_grad_(True)
     out = sb.signature(xt, N)
+    L0 = sb.lib().sig_launch_count()
     out.backward(_cuda(g))
+    torch.cuda.synchronize()
+    n_saved = sb.lib().sig_launch_count() - L0
     ref_out = sb.sig_signature(xt.detach(), N)
+    L1 = sb.lib().sig_launch_count()
     gp2, _ = sb.sig_signature_backward(_cuda(g), xt.detach(), out.detach(), N)
+    n_recompute = sb.lib().sig_launch_count() - L1
     assert torch.equal(xt.grad, gp2)
+    assert n_saved < n_recompute, (n_saved, n_recompute)  # no chunk-signature pass, no prefix scan
     assert level_rel_err(out.detach().cpu().numpy(), ref_out.cpu().numpy(), C, N) < FWD_TOL
 
 
