@@ -28,6 +28,14 @@
 #ifndef SIG_FWD_TMA_STAGE
 #define SIG_FWD_TMA_STAGE 1
 #endif
+// one-prefix forward prefix chains written as b * (z_p / m) + A instead of (b / m) z_p + A (same
+// operation count; measured: c5's scan 410 -> 400 us; the two-prefix mulexp2 keeps the other form:
+// c2's forward 237 -> 243 us with it).  The backward's reversal keeps the other form: there
+// the scaled increments become common subexpressions of the reversal, the VJP chains and the low
+// tails, and the extra live registers measured slower (c5b +1.6%, c4 +0.4%).
+#ifndef SIG_ZS_CSE
+#define SIG_ZS_CSE 1
+#endif
 
 namespace sigb200 {
 
@@ -116,6 +124,7 @@ __device__ __forceinline__ float prefix_chain(const float (&own)[SZ], const floa
         if constexpr (i < P) Ai = low[i];
         else Ai = own[SH::own_off(P)];
         if constexpr (i == 1) b = fmaf(zp[0], sg * inv_int(K), Ai);
+        else if constexpr (SIG_ZS_CSE && !NEG) b = fmaf(b, zp[i - 1] * inv_int(K - i + 1), Ai);
         else b = fmaf(b * (sg * inv_int(K - i + 1)), zp[i - 1], Ai);
     });
     return b;
@@ -142,6 +151,7 @@ __device__ __forceinline__ void fused_mulexp(float (&own)[SZ], float (&low)[SH::
         static_for<1, k + 1>([&](auto ic) {
             constexpr int i = decltype(ic)::value;
             if constexpr (i == 1) b = fmaf(zp[0], sg * inv_int(k), low[i]);
+            else if constexpr (SIG_ZS_CSE && !NEG) b = fmaf(b, zp[i - 1] * inv_int(k - i + 1), low[i]);
             else b = fmaf(b * (sg * inv_int(k - i + 1)), zp[i - 1], low[i]);
         });
         low[k] = b;
