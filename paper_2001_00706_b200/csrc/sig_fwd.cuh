@@ -33,6 +33,12 @@
 // c2's forward 237 -> 243 us with it).  The backward's reversal keeps the other form: there
 // the scaled increments become common subexpressions of the reversal, the VJP chains and the low
 // tails, and the extra live registers measured slower (c5b +1.6%, c4 +0.4%).
+// threads of the blocked chunk scan's CTA (one group of up to 16 chunk signatures, scanned in
+// order with one barrier per element): 1024 puts about one coefficient of each product on a thread
+// (c5b: ~2.4 us less per scan launch than with 512, 10 launches per step)
+#ifndef SIG_SCAN_THREADS
+#define SIG_SCAN_THREADS 1024
+#endif
 #ifndef SIG_ZS_CSE
 #define SIG_ZS_CSE 1
 #endif
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(512) fold_group_t_kernel(const GroupParams p) 
 //   prefix: Y_0 = E [x] X_0, Y_i = Y_{i-1} [x] X_i;   suffix: Y_{n-1} = X_{n-1} [x] E, Y_i = X_i [x] Y_{i+1}.
 // Writes Y to out (if given) and the group total (prefix: Y_{n-1}, suffix: Y_0) to tot[b, grp].
 template <class SH>
-__global__ void __launch_bounds__(512) scan_group_t_kernel(const ScanParams p) {
+__global__ void __launch_bounds__(SIG_SCAN_THREADS) scan_group_t_kernel(const ScanParams p) {
     extern __shared__ __align__(16) float ss[];  // X[g][S], Y[g][S], E[S]
     constexpr int S = (int)SH::S;
     const int g = p.g;
@@ -421,7 +427,7 @@ cudaError_t launch_scan_group_t(const ScanParams& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;
     }
     const int64_t ng = (p.m + p.g - 1) / p.g;
-    scan_group_t_kernel<SH><<<dim3((unsigned)ng, p.B < 65535 ? (unsigned)p.B : 65535u), 512, smem, st>>>(p);
+    scan_group_t_kernel<SH><<<dim3((unsigned)ng, p.B < 65535 ? (unsigned)p.B : 65535u), SIG_SCAN_THREADS, smem, st>>>(p);
     return cudaGetLastError();
 }
 
