@@ -81,12 +81,16 @@ struct FwdPlan {
     size_t ws_bytes;
 };
 
+#ifndef SIG_FOLD_G
+#define SIG_FOLD_G 8
+#endif
 int group_size_for(int64_t S, bool compiled) {
     if (compiled) {
-        // compiled fold (fold_group_t_kernel, one barrier per tree level, 512 threads): small groups
-        // and many CTAs per level -- each CTA's fold is latency-bound (c5, 740 partials: G = 4, 8,
-        // 16 measured 432, 435, 444 us for the whole signature)
-        int G = 4;
+        // compiled fold (fold_group_t_kernel, one barrier per tree level): each CTA's fold is
+        // latency-bound (c5, 740 partials, 512 threads: G = 4, 8, 16 measured 432, 435, 444 us for
+        // the whole signature; 1480 partials: G = 8 with 1024 threads 390 us against 400 for G = 4
+        // with 512)
+        int G = SIG_FOLD_G;
         while (G > 2 && (size_t)(G + (G + 1) / 2) * S * sizeof(float) > 200 * 1024) G >>= 1;
         if ((size_t)(G + (G + 1) / 2) * S * sizeof(float) <= 200 * 1024) return G;
         return 0;

@@ -36,6 +36,11 @@
 // threads of the blocked chunk scan's CTA (one group of up to 16 chunk signatures, scanned in
 // order with one barrier per element): 1024 puts about one coefficient of each product on a thread
 // (c5b: ~2.4 us less per scan launch than with 512, 10 launches per step)
+// threads of the compiled group fold (K3) CTA; with groups of SIG_FOLD_G = 8 (api.cu): c5's six
+// fold launches of 512-thread CTAs in groups of 4 become four, forward 400 -> 390 us
+#ifndef SIG_FOLD_THREADS
+#define SIG_FOLD_THREADS 1024
+#endif
 #ifndef SIG_SCAN_THREADS
 #define SIG_SCAN_THREADS 1024
 #endif
@@ -341,7 +346,7 @@ __device__ __forceinline__ const float* block_fold_t(float* gs, float* tmp, int 
 // K3 group fold compiled per shape: CTA (g, b) folds elements g*G .. g*G+G-1 of path b in time
 // order (block_fold_t: one barrier per tree level) -- the fold of the time-chunk partials.
 template <class SH>
-__global__ void __launch_bounds__(512) fold_group_t_kernel(const GroupParams p) {
+__global__ void __launch_bounds__(SIG_FOLD_THREADS) fold_group_t_kernel(const GroupParams p) {
     extern __shared__ __align__(16) float gs[];  // [G][S] + [ceil(G/2)][S]
     constexpr int S = (int)SH::S;
     const int64_t g = blockIdx.x;
@@ -439,7 +444,7 @@ cudaError_t launch_fold_group_t(const GroupParams& p, unsigned ngroups, unsigned
         cudaError_t e = cudaFuncSetAttribute(fold_group_t_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    fold_group_t_kernel<SH><<<dim3(ngroups, B < 65535u ? B : 65535u), 512, smem, st>>>(p);
+    fold_group_t_kernel<SH><<<dim3(ngroups, B < 65535u ? B : 65535u), SIG_FOLD_THREADS, smem, st>>>(p);
     return cudaGetLastError();
 }
 
