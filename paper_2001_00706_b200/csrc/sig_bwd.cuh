@@ -111,6 +111,10 @@ __device__ __forceinline__ void stage_path_increments(const BwdParams& prm, int6
 #ifndef SIG_BWD_GNS
 #define SIG_BWD_GNS 0
 #endif
+// one-warp backward CTAs (small states, e.g. C=3, N=6) resident per SM (registers <= 64K / (32 n))
+#ifndef SIG_BWD_WARP_CTAS
+#define SIG_BWD_WARP_CTAS 16
+#endif
 #ifndef SIG_BWD_GNS_MAXKB
 #define SIG_BWD_GNS_MAXKB 96
 #endif
@@ -143,7 +147,7 @@ struct BwdLayout {
     static constexpr bool GNS = SIG_BWD_GNS && (C % 4 == 0) && (SH::own(N) >= 16) && (SH::CP % 32 == 0) &&
                                 (SH::P > 0) && ((size_t)NT * SH::own(N) * 4 <= SIG_BWD_GNS_MAXKB * 1024);
     static constexpr int GNF = GNS ? NT * SH::own(N) : 0;  // floats of the G_N region
-    static constexpr int MINB = (NT == 32 && SH::OWN + SH::OWNA <= 64) ? 16 : (GNS ? SIG_BWD_GNS_MINB : 1);
+    static constexpr int MINB = (NT == 32 && SH::OWN + SH::OWNA <= 64) ? SIG_BWD_WARP_CTAS : (GNS ? SIG_BWD_GNS_MINB : 1);
     static constexpr int RECS = FAST ? HW : NT;      // records per step
     // shared memory of a tile of T steps: the tile's increments, T + 1 record slots, the per-step
     // totals, gprev, and the low-level partials of grad_initial
