@@ -81,6 +81,9 @@ struct FwdPlan {
     size_t ws_bytes;
 };
 
+#ifndef SIG_FWD_GROUP_THREADS
+#define SIG_FWD_GROUP_THREADS 256
+#endif
 #ifndef SIG_FOLD_G
 #define SIG_FOLD_G 8
 #endif
@@ -175,7 +178,7 @@ sig_status_t make_fwd_plan(int64_t B, int64_t L, int64_t C, int32_t depth, int32
         const int cp = (int)sigb200::ipow(C, pl.P);
         // ~256-thread CTAs: two or more resident per SM, so one CTA's staging and fold phases
         // overlap another's scan (c5: 9 chunks of 27 threads, 506 -> 474 us vs 18 per CTA)
-        int upc = cp <= 256 ? 256 / cp : 0;
+        int upc = cp <= SIG_FWD_GROUP_THREADS ? SIG_FWD_GROUP_THREADS / cp : 0;
         if (upc > 32) upc = 32;
         while (upc >= 2 && (size_t)(upc + (upc + 1) / 2) * S * sizeof(float) > 200 * 1024) --upc;
         if (upc >= 2) {
