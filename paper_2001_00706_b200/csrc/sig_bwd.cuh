@@ -93,10 +93,11 @@ __device__ __forceinline__ void stage_path_increments(const BwdParams& prm, int6
     }
 }
 
-// Per-step gz records are flushed every T steps (a CTA barrier each time).  With up to 128 steps
-// per tile a c2/c4 path has a single flush, so the warps run the whole reversal without a barrier.
+// Per-step gz records are flushed every T steps (a CTA barrier each time).  With up to 256 steps
+// per tile a c2/c4 path has a single flush, so the warps run the whole reversal without a barrier
+// (c4's 255 steps: 128-step tiles 679 us, one 256-step tile 677 us).
 #ifndef SIG_BWD_TMAX
-#define SIG_BWD_TMAX 128
+#define SIG_BWD_TMAX 256
 #endif
 #ifndef SIG_BWD_TILE_KB
 #define SIG_BWD_TILE_KB 160
